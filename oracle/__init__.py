@@ -1,0 +1,200 @@
+"""PCDM1/LASSO serial CPU oracle (ctypes wrapper around oracle/pcdm_oracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product package ``paper_1212_0873_b200`` never imports it and
+shares no code with it ("Oracle").
+
+Every function follows the paper step by step in fp64; the C source cites the
+PAPER.md lines for each step.  Array arguments are numpy arrays on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pcdm_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc -O2 (no fast-math, no OpenMP, no intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp.%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-D_POSIX_C_SOURCE=199309L", "-fPIC",
+                               "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    build()
+    lib = ctypes.CDLL(_LIB)
+    P = ctypes.c_void_p
+    i64, u64, u32, f64, i32 = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32,
+                               ctypes.c_double, ctypes.c_int)
+    lib.or_philox4x32_10.argtypes = [P, P, P]
+    lib.or_philox4x32_10.restype = None
+    lib.or_draw.argtypes = [u64, u32, u32, u32, u32, u64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.or_draw.restype = i32
+    lib.or_sample.argtypes = [u64, i64, i64, i64, P, P]
+    lib.or_sample.restype = i32
+    lib.or_row_counts.argtypes = [i64, P, P]
+    lib.or_row_counts.restype = None
+    lib.or_omega.argtypes = [i64, i64, P]
+    lib.or_omega.restype = i64
+    lib.or_col_norms.argtypes = [i64, P, P, P]
+    lib.or_col_norms.restype = None
+    lib.or_beta.argtypes = [i64, i64, i64]
+    lib.or_beta.restype = f64
+    lib.or_prox.argtypes = [f64, f64, f64, f64]
+    lib.or_prox.restype = f64
+    lib.or_residual.argtypes = [i64, i64, P, P, P, P, P, P]
+    lib.or_residual.restype = None
+    lib.or_objective.argtypes = [i64, i64, P, P, P, P, f64, P]
+    lib.or_objective.restype = f64
+    lib.or_refresh_period.argtypes = [i64, i64, i64]
+    lib.or_refresh_period.restype = i64
+    lib.or_run.argtypes = [i64, i64, P, P, P, P, f64, P, f64, P, i64, i64, u64, i64, i64,
+                           P, P, ctypes.POINTER(ctypes.c_double)]
+    lib.or_run.restype = i32
+    _lib = lib
+    return lib
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _csc(colptr, rowidx, val):
+    colptr = np.ascontiguousarray(colptr, dtype=np.int64)
+    rowidx = np.ascontiguousarray(rowidx, dtype=np.int32)
+    val = np.ascontiguousarray(val, dtype=np.float32)
+    return colptr, rowidx, val
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    _load().or_philox4x32_10(_ptr(c), _ptr(k), _ptr(out))
+    return out
+
+
+def draw(seed: int, k: int, rho: int, j: int, tag: int, n: int):
+    """One Lemire-mapped draw; returns the value in [0,n) or None if rejected."""
+    v = ctypes.c_uint64(0)
+    ok = _load().or_draw(seed, k, rho, j, tag, n, ctypes.byref(v))
+    return int(v.value) if ok else None
+
+
+def sample(seed: int, k: int, tau: int, n: int) -> np.ndarray:
+    """O5: slot array of S_k (tau distinct indices in [0, n))."""
+    out = np.empty(tau, dtype=np.int32)
+    rc = _load().or_sample(seed, k, tau, n, _ptr(out), None)
+    if rc != 0:
+        raise ValueError("or_sample failed (rc=%d)" % rc)
+    return out
+
+
+def row_counts(m: int, rowidx) -> np.ndarray:
+    rowidx = np.ascontiguousarray(rowidx, dtype=np.int32)
+    counts = np.zeros(m, dtype=np.int64)
+    _load().or_row_counts(rowidx.size, _ptr(rowidx), _ptr(counts))
+    return counts
+
+
+def omega(m: int, rowidx) -> int:
+    """O1: max stored entries in any row."""
+    rowidx = np.ascontiguousarray(rowidx, dtype=np.int32)
+    return int(_load().or_omega(m, rowidx.size, _ptr(rowidx)))
+
+
+def col_norms(colptr, val) -> np.ndarray:
+    """O2: L_i = ||a_i||^2 in fp64."""
+    colptr = np.ascontiguousarray(colptr, dtype=np.int64)
+    val = np.ascontiguousarray(val, dtype=np.float32)
+    n = colptr.size - 1
+    L = np.empty(n, dtype=np.float64)
+    _load().or_col_norms(n, _ptr(colptr), _ptr(val), _ptr(L))
+    return L
+
+
+def beta(omega_: int, tau: int, n: int) -> float:
+    """O3: beta = 1 + (omega-1)(tau-1)/max(1,n-1)."""
+    return float(_load().or_beta(omega_, tau, n))
+
+
+def prox(x: float, g: float, s: float, lam: float) -> float:
+    """Soft-threshold block update: returns x+ = x + h_i."""
+    return float(_load().or_prox(x, g, s, lam))
+
+
+def residual(m, colptr, rowidx, val, b, x) -> np.ndarray:
+    """O4: r = Ax - b in fp64."""
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    r = np.empty(m, dtype=np.float64)
+    _load().or_residual(m, colptr.size - 1, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(b),
+                        _ptr(x), _ptr(r))
+    return r
+
+
+def objective(m, colptr, rowidx, val, b, lam, x) -> float:
+    """F(x) = 1/2||Ax-b||^2 + lambda||x||_1 in fp64."""
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return float(_load().or_objective(m, colptr.size - 1, _ptr(colptr), _ptr(rowidx), _ptr(val),
+                                      _ptr(b), lam, _ptr(x)))
+
+
+def refresh_period(n: int, tau: int, refresh_every: int = 0) -> int:
+    return int(_load().or_refresh_period(n, tau, refresh_every))
+
+
+class RunResult:
+    __slots__ = ("x", "r", "slots", "loop_seconds", "omega", "beta", "L")
+
+    def __init__(self, x, r, slots, loop_seconds, omega_, beta_, L):
+        self.x, self.r, self.slots, self.loop_seconds = x, r, slots, loop_seconds
+        self.omega, self.beta, self.L = omega_, beta_, L
+
+
+def run(m, colptr, rowidx, val, b, lam, tau, iters, seed, x0=None, first_iter=0,
+        refresh_every=0, beta_override=None, omega_override=None, L=None,
+        keep_slots=False) -> RunResult:
+    """Synchronous PCDM1 (alg:PCD1) for LASSO, O1..O8 of SURVEY 8(c).
+
+    omega_override / L let a caller hand in the oracle's own omega / L computed
+    on a larger matrix (sub-instance runs); they never come from the GPU path.
+    """
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    n = colptr.size - 1
+    lib = _load()
+    om = omega(m, rowidx) if omega_override is None else int(omega_override)
+    Lv = col_norms(colptr, val) if L is None else np.ascontiguousarray(L, dtype=np.float64)
+    bt = beta(om, tau, n) if beta_override is None else float(beta_override)
+    x = np.zeros(n, dtype=np.float64) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    r = np.empty(m, dtype=np.float64)
+    slots = np.empty(iters * tau, dtype=np.int32) if keep_slots else None
+    secs = ctypes.c_double(0.0)
+    rc = lib.or_run(m, n, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(b), lam, _ptr(Lv), bt,
+                    _ptr(x), tau, iters, seed, first_iter, refresh_every, _ptr(r),
+                    _ptr(slots) if keep_slots else None, ctypes.byref(secs))
+    if rc < 0:
+        raise ValueError("or_run failed (rc=%d)" % rc)
+    if rc == 1:
+        raise FloatingPointError("oracle: non-finite delta (diverged)")
+    return RunResult(x, r, slots.reshape(iters, tau) if keep_slots else None, secs.value, om, bt, Lv)

@@ -1,0 +1,227 @@
+"""Seeded synthetic LASSO instances shaped like the paper's workloads.
+
+This module only builds INPUTS (A in CSC, b, lambda, the planted x*); it holds
+none of the method's arithmetic and is the one module both the CUDA path's
+tests/bench and the oracle's tests draw from ("Input recipe").
+
+Recipe (BASELINE.json ``configs``), standing in for the
+paper's 10^9-variable instance of Sec. 8.1, whose
+"modified primal-dual generator" and 350 GB size are not reproducible here:
+
+  G1  each column gets ``c`` distinct rows, uniform or Zipf(s) over rows
+      (P(row = j-1) ~ j^-s, hot rows at low indices), sorted ascending;
+  G2  values iid N(0,1), fp32, in sorted-row order;
+  G3  x* has ``s_star`` distinct uniform positions with N(0,1) values;
+  G4  b = fp32(A x* (fp64 accumulation) + 0.01 * eps), eps iid N(0,1);
+  G5  lambda = 0.1 * max_i |a_i^T b| (fp64, on the fp32 b);
+  G6  x0 = 0.
+
+Randomness comes from a ``torch.Generator`` seeded with ``seed`` on
+``device``; an instance is a deterministic function of (config, seed, device
+type).  Parity tests always hand the SAME arrays to both sides.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Optional
+
+import torch
+
+
+@dataclasses.dataclass(frozen=True)
+class InstanceConfig:
+    name: str
+    m: int
+    n: int
+    nnz_per_col: int
+    s_star: int
+    rows: str = "uniform"      # "uniform" | "zipf"
+    zipf_s: float = 1.1
+    noise: float = 0.01
+    lam_frac: float = 0.1
+    tau: int = 1
+    iters: int = 1
+
+
+# BASELINE.json "configs", in order.
+CONFIGS = {
+    "tiny": InstanceConfig("tiny", 2000, 1000, 10, 100, tau=32, iters=2000),
+    "medium": InstanceConfig("medium", 100_000, 100_000, 20, 1000, tau=1024, iters=10_000),
+    "skewed": InstanceConfig("skewed", 1_000_000, 1_000_000, 20, 10_000, rows="zipf",
+                             tau=1 << 12, iters=10_000),
+    "large": InstanceConfig("large", 2_000_000, 10_000_000, 20, 10_000, tau=65536, iters=2000),
+    "huge": InstanceConfig("huge", 100_000_000, 500_000_000, 10, 100_000, tau=1 << 18, iters=500),
+}
+SKEWED_TAUS = [1 << e for e in range(8, 17)]
+
+
+@dataclasses.dataclass
+class Instance:
+    cfg: InstanceConfig
+    m: int
+    n: int
+    colptr: torch.Tensor   # int64[n+1]
+    rowidx: torch.Tensor   # int32[nnz]
+    val: torch.Tensor      # float32[nnz]
+    b: torch.Tensor        # float32[m]
+    lam: float
+    xstar_idx: torch.Tensor
+    xstar_val: torch.Tensor
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rowidx.numel())
+
+    def to(self, device) -> "Instance":
+        return dataclasses.replace(
+            self, colptr=self.colptr.to(device), rowidx=self.rowidx.to(device),
+            val=self.val.to(device), b=self.b.to(device),
+            xstar_idx=self.xstar_idx.to(device), xstar_val=self.xstar_val.to(device))
+
+    def numpy(self):
+        """Host numpy views (colptr, rowidx, val, b) for the oracle."""
+        return (self.colptr.cpu().numpy(), self.rowidx.cpu().numpy(),
+                self.val.cpu().numpy(), self.b.cpu().numpy())
+
+
+def _zipf_cdf(m: int, s: float, device) -> torch.Tensor:
+    j = torch.arange(1, m + 1, dtype=torch.float64, device=device)
+    w = j.pow(-s)
+    cdf = torch.cumsum(w, 0)
+    return cdf / cdf[-1]
+
+
+def _draw_rows(k: int, c: int, m: int, gen, device, zipf_cdf: Optional[torch.Tensor]):
+    """k columns x c distinct rows each, sorted ascending (G1), int64."""
+    def fresh(count):
+        if zipf_cdf is None:
+            return torch.randint(0, m, (count,), generator=gen, device=device, dtype=torch.int64)
+        u = torch.rand(count, generator=gen, device=device, dtype=torch.float64)
+        return torch.searchsorted(zipf_cdf, u, right=True).clamp_(max=m - 1)
+
+    rows = fresh(k * c).view(k, c)
+    rows, _ = torch.sort(rows, dim=1)
+    while True:
+        dup = torch.zeros_like(rows, dtype=torch.bool)
+        dup[:, 1:] = rows[:, 1:] == rows[:, :-1]
+        nd = int(dup.sum())
+        if nd == 0:
+            return rows
+        rows[dup] = fresh(nd)
+        rows, _ = torch.sort(rows, dim=1)
+
+
+def generate(cfg: InstanceConfig | str, seed: int = 0, device="cpu",
+             chunk_cols: int = 1 << 23) -> Instance:
+    """Build the instance of ``cfg`` (a name from CONFIGS or an InstanceConfig)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    device = torch.device(device)
+    m, n, c = cfg.m, cfg.n, cfg.nnz_per_col
+    if not (1 <= c <= m):
+        raise ValueError("need 1 <= nnz_per_col <= m")
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    nnz = n * c
+    rowidx = torch.empty(nnz, dtype=torch.int32, device=device)
+    val = torch.empty(nnz, dtype=torch.float32, device=device)
+    zcdf = _zipf_cdf(m, cfg.zipf_s, device) if cfg.rows == "zipf" else None
+    for c0 in range(0, n, chunk_cols):
+        k = min(chunk_cols, n - c0)
+        rows = _draw_rows(k, c, m, gen, device, zcdf)
+        rowidx[c0 * c:(c0 + k) * c] = rows.view(-1).to(torch.int32)
+        del rows
+        val[c0 * c:(c0 + k) * c] = torch.randn(k * c, generator=gen, device=device,
+                                               dtype=torch.float32)
+    colptr = torch.arange(0, n + 1, dtype=torch.int64, device=device) * c
+
+    # G3: planted support
+    s = min(cfg.s_star, n)
+    idx = torch.empty(0, dtype=torch.int64, device=device)
+    while idx.numel() < s:
+        more = torch.randint(0, n, (2 * s,), generator=gen, device=device, dtype=torch.int64)
+        idx = torch.unique(torch.cat([idx, more]))
+    perm = torch.randperm(idx.numel(), generator=gen, device=device)[:s]
+    xs_idx = torch.sort(idx[perm]).values
+    xs_val = torch.randn(s, generator=gen, device=device, dtype=torch.float64)
+
+    # G4: b = fp32(A x* + noise * eps), fp64 accumulation
+    b64 = torch.zeros(m, dtype=torch.float64, device=device)
+    pos = (xs_idx.view(-1, 1) * c + torch.arange(c, device=device).view(1, -1)).view(-1)
+    contrib = val[pos].to(torch.float64) * xs_val.repeat_interleave(c)
+    b64.index_add_(0, rowidx[pos].to(torch.int64), contrib)
+    b64 += cfg.noise * torch.randn(m, generator=gen, device=device, dtype=torch.float64)
+    b = b64.to(torch.float32)
+
+    # G5: lambda = lam_frac * ||A^T b||_inf (fp64 on the fp32 b)
+    bd = b.to(torch.float64)
+    amax = 0.0
+    for c0 in range(0, n, chunk_cols):
+        k = min(chunk_cols, n - c0)
+        sl = slice(c0 * c, (c0 + k) * c)
+        atb = (val[sl].to(torch.float64) * bd[rowidx[sl].to(torch.int64)]).view(k, c).sum(1)
+        amax = max(amax, float(atb.abs().max()))
+    lam = cfg.lam_frac * amax
+    return Instance(cfg, m, n, colptr, rowidx, val, b, lam, xs_idx, xs_val.to(torch.float32))
+
+
+def random_csc(m: int, n: int, col_lengths, seed: int = 0, device="cpu",
+               values: str = "normal"):
+    """Small ragged CSC for edge-case tests: column i gets col_lengths[i]
+    distinct uniform rows (sorted).  Returns (colptr int64, rowidx int32, val f32)."""
+    gen = torch.Generator(device="cpu")
+    gen.manual_seed(seed)
+    lens = [int(v) for v in col_lengths]
+    rows, vals = [], []
+    for ln in lens:
+        if ln > m:
+            raise ValueError("column longer than m")
+        r = torch.randperm(m, generator=gen)[:ln].sort().values
+        rows.append(r)
+        if values == "normal":
+            vals.append(torch.randn(ln, generator=gen, dtype=torch.float32))
+        else:
+            vals.append(torch.ones(ln, dtype=torch.float32))
+    colptr = torch.zeros(n + 1, dtype=torch.int64)
+    colptr[1:] = torch.cumsum(torch.tensor(lens, dtype=torch.int64), 0)
+    rowidx = torch.cat(rows).to(torch.int32) if rows else torch.zeros(0, dtype=torch.int32)
+    val = torch.cat(vals) if vals else torch.zeros(0, dtype=torch.float32)
+    return colptr.to(device), rowidx.to(device), val.to(device)
+
+
+def random_b(m: int, seed: int = 0, device="cpu") -> torch.Tensor:
+    gen = torch.Generator(device="cpu")
+    gen.manual_seed(seed + 7919)
+    return torch.randn(m, generator=gen, dtype=torch.float32).to(device)
+
+
+def lam_for(colptr, rowidx, val, b, frac: float = 0.1) -> float:
+    """G5 on an arbitrary small CSC (host tensors)."""
+    n = colptr.numel() - 1
+    col = torch.repeat_interleave(torch.arange(n), (colptr[1:] - colptr[:-1]))
+    atb = torch.zeros(n, dtype=torch.float64)
+    atb.index_add_(0, col, val.double() * b.double()[rowidx.long()])
+    return frac * float(atb.abs().max()) if n else 0.0
+
+
+def equal_row_01_matrix(m: int, n: int, omega: int, seed: int = 0):
+    """0-1 matrix with exactly ``omega`` ones per row and k = omega*m/n ones per
+    column (the DSO tightness construction).  Rows are
+    consecutive cyclic windows of a random column permutation; requires
+    omega*m % n == 0.  Returns a host CSC (colptr, rowidx, val)."""
+    if (omega * m) % n:
+        raise ValueError("need omega*m divisible by n")
+    gen = torch.Generator(device="cpu")
+    gen.manual_seed(seed)
+    perm = torch.randperm(n, generator=gen)
+    cols = [[] for _ in range(n)]
+    for j in range(m):
+        for t in range(omega):
+            cols[int(perm[(j * omega + t) % n])].append(j)
+    lens = [len(cl) for cl in cols]
+    colptr = torch.zeros(n + 1, dtype=torch.int64)
+    colptr[1:] = torch.cumsum(torch.tensor(lens), 0)
+    rowidx = torch.tensor([r for cl in cols for r in sorted(cl)], dtype=torch.int32)
+    val = torch.ones(rowidx.numel(), dtype=torch.float32)
+    return colptr, rowidx, val
