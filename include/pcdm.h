@@ -1,0 +1,170 @@
+/*
+ * pcdm.h -- C ABI of libpcdm.so, the B200 (sm_100a) hot path of synchronous
+ * PCDM1 (parallel coordinate descent, arXiv 1212.0873) on LASSO:
+ *
+ *     minimise  F(x) = 1/2 ||A x - b||^2 + lambda ||x||_1          (eq:P, PAPER.md:42-46;
+ *                                                                     LASSO instance PAPER.md:1175)
+ *
+ * One PCDM1 iteration (alg:PCD1):
+ *   draw a tau-nice sampling S_k (tau distinct coordinates, uniformly at random,
+ *   PAPER.md:436-438); for each i in S_k, from the SAME snapshot r_k = A x_k - b:
+ *     g_i = a_i^T r_k                                  (grad_i f)
+ *     x_i+ = argmin_t g_i t + (beta L_i / 2) t^2 + lambda |x_i + t|  (+ x_i)
+ *                                                      (eq:h(x) block form PAPER.md:214-216)
+ *   with w = L, L_i = ||a_i||^2 and the tau-nice ESO constant
+ *     beta = 1 + (omega - 1)(tau - 1) / max(1, n - 1)  (thm:ESO-nice PAPER.md:875-878),
+ *     omega = max_j ||A_j||_0 (stored entries per row);
+ *   then x_i <- x_i+ and r <- r + (x_i+ - x_i) a_i for all i in S_k.
+ *
+ * Conventions for every entry point
+ *   - Array pointers may be HOST or DEVICE memory (CUDA device/managed pointers
+ *     are used in place; host pointers, pinned or pageable, are copied).  The
+ *     library detects which with cudaPointerGetAttributes.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All device work
+ *     is enqueued on it.
+ *   - Errors: every call returns a pcdm_status; nothing is thrown across the ABI.
+ *     pcdm_last_error() returns a thread-local message for the last failing call.
+ *   - Handles are not thread-safe; distinct handles are independent.
+ *   - Sizes: 1 <= m < 2^31 (int32 row indices), 1 <= n < 2^31, 1 <= nnz < 2^62.
+ */
+#ifndef PCDM_H
+#define PCDM_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PCDM_API __attribute__((visibility("default")))
+#else
+#define PCDM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pcdm_problem pcdm_problem; /* opaque, owned by the library */
+
+typedef enum {
+    PCDM_OK = 0,
+    PCDM_EINVAL = 1,    /* bad argument or malformed CSC / non-finite input   */
+    PCDM_ENOMEM = 2,    /* device allocation failed                           */
+    PCDM_ECUDA = 3,     /* any other CUDA runtime failure                     */
+    PCDM_EDIVERGED = 4, /* a non-finite step occurred during pcdm_run          */
+    PCDM_ESAMPLER = 5   /* sampler round counter overflow (never in practice) */
+} pcdm_status;
+
+/* Execution variants of the iteration loop (pcdm_run_ex).  All compute the same
+ * synchronous PCDM1 iteration; they differ only in where the barrier between the
+ * read phase (all g_i of S_k from r_k) and the write phase (r += delta_i a_i)
+ * runs and where the data lives. */
+typedef enum {
+    PCDM_VARIANT_AUTO = 0, /* pick by problem size                                      */
+    PCDM_VARIANT_GRID = 1, /* persistent cooperative grid, r in HBM/L2, grid barriers    */
+    PCDM_VARIANT_SMEM = 2, /* one CTA, A, r, x, L resident in shared memory (small A)    */
+    PCDM_VARIANT_BLOCK = 3 /* one CTA, data in HBM/L2, __syncthreads barriers            */
+} pcdm_variant;
+
+typedef struct {
+    int64_t iters;              /* iterations executed by the last run              */
+    int64_t nonzero_deltas;     /* number of (i in S_k, k) with delta_i != 0        */
+    int64_t sampler_max_rounds; /* largest sampler round index used + 1            */
+    int64_t refreshes;          /* residual refreshes performed (excl. the initial) */
+    int64_t kernel_launches;    /* kernels of this library launched by the run      */
+    int32_t variant;            /* pcdm_variant actually used                       */
+    int32_t grid_ctas;          /* CTAs of the iteration kernel                     */
+    int32_t threads_per_cta;
+    int32_t lanes_per_column;   /* threads cooperating on one sampled column        */
+    int64_t chunk_iters;        /* iterations per iteration-kernel launch (max)     */
+    int64_t iter_launches;      /* launches of the iteration kernel                 */
+    double iter_kernel_ms;      /* summed device time of the iteration kernel       */
+    double sampler_ms;          /* summed device time of the sampler passes         */
+    double setup_ms;            /* residual init/refresh + copies (device time)     */
+} pcdm_run_stats;
+
+/* pcdm_create -- build a problem handle for LASSO with A (m x n, CSC), b, lambda.
+ *   colptr int64[n+1], rowidx int32[nnz], val float32[nnz]: CSC of A, column i has
+ *     entries p in [colptr[i], colptr[i+1]); rows strictly increasing per column.
+ *   b float32[m]; lambda >= 0 finite.
+ * The library copies (and may repack) everything into its own device memory; the
+ * caller may free its arrays when the call returns (the call synchronises `stream`).
+ * Computes L_i = ||a_i||^2 (fp64 accumulation, stored fp32) and
+ * omega = max row count.
+ * Errors: EINVAL for m,n,nnz < 1, colptr[0] != 0, colptr[n] != nnz, decreasing
+ * colptr, row index out of [0,m) or not strictly increasing within a column,
+ * non-finite val or b, lambda < 0 or non-finite, NULL pointers. */
+PCDM_API pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t *colptr,
+                        const int32_t *rowidx, const float *val, const float *b, double lambda,
+                        void *stream, pcdm_problem **out);
+
+/* Frees every device buffer of the handle (NULL is a no-op). */
+PCDM_API void pcdm_destroy(pcdm_problem *p);
+
+/* Thread-local message describing the most recent failure (never NULL). */
+PCDM_API const char *pcdm_last_error(void);
+
+/* Degree of partial separability omega (host value cached at create). */
+PCDM_API pcdm_status pcdm_omega(const pcdm_problem *p, int64_t *omega);
+
+/* beta = 1 + (omega-1)(tau-1)/max(1,n-1) in fp64 (thm:ESO-nice). EINVAL if tau not in [1,n]. */
+PCDM_API pcdm_status pcdm_beta(const pcdm_problem *p, int64_t tau, double *beta);
+
+/* pcdm_run -- `iters` synchronous PCDM1 iterations k = 0..iters-1 with the
+ * tau-nice sampling keyed by `seed`, starting from x (float32[n], in/out).
+ * Equivalent to pcdm_run_ex(p, x, tau, iters, seed, 0, 0, 0.0, PCDM_VARIANT_AUTO, stream).
+ * x is read at the start and written at the end (device x is updated in place).
+ * Synchronises `stream` once after the initial residual and once at the end.
+ * Errors: EINVAL for tau not in [1,n], iters < 0, non-finite x; EDIVERGED if a
+ * step was non-finite (x then holds the diverged iterate). */
+PCDM_API pcdm_status pcdm_run(pcdm_problem *p, float *x, int64_t tau, int64_t iters, uint64_t seed,
+                     void *stream);
+
+/* pcdm_run_ex -- pcdm_run with the knobs the tests and the bench need:
+ *   first_iter    iteration index of the first step (resume: the sampler stream
+ *                 continues bit-exactly); first_iter + iters <= 2^32.
+ *   refresh_every residual r = Ax - b recomputed from scratch after every R-th
+ *                 iteration (fp64 accumulation): 0 = default R = ceil(2n/tau),
+ *                 -1 = never, > 0 = that R.  (reading R#8.)
+ *   beta_override > 0 replaces the formula's beta (ESO inflation).
+ *   variant       pcdm_variant. */
+PCDM_API pcdm_status pcdm_run_ex(pcdm_problem *p, float *x, int64_t tau, int64_t iters, uint64_t seed,
+                        int64_t first_iter, int64_t refresh_every, double beta_override,
+                        int32_t variant, void *stream);
+
+/* F(x) = 1/2||Ax-b||^2 + lambda||x||_1, residual accumulated in fp64 from scratch,
+ * sums in fp64 (eq:P). x float32[n] host or device. Synchronises `stream`. */
+PCDM_API pcdm_status pcdm_objective(pcdm_problem *p, const float *x, double *F, void *stream);
+
+/* Statistics of the most recent pcdm_run / pcdm_run_ex on this handle. */
+PCDM_API pcdm_status pcdm_last_run_stats(const pcdm_problem *p, pcdm_run_stats *stats);
+
+/* ---- test and measurement hooks (not the hot path) ---------------------- */
+
+/* Slot arrays of S_k for k = first_iter .. first_iter+count-1 (int32[count*tau],
+ * row-major by k), exactly as pcdm_run draws them.  1 <= tau <= n < 2^31. */
+PCDM_API pcdm_status pcdm_sample(int64_t n, int64_t tau, uint64_t seed, int64_t first_iter, int64_t count,
+                        int32_t *slots, void *stream);
+
+/* L_i = ||a_i||^2 as stored by the library (float32[n]). */
+PCDM_API pcdm_status pcdm_col_norms(const pcdm_problem *p, float *L, void *stream);
+
+/* Row histogram counts[j] = #stored entries in row j (int32[m]); omega = max. */
+PCDM_API pcdm_status pcdm_row_counts(const pcdm_problem *p, int32_t *counts, void *stream);
+
+/* The maintained residual r (float32[m]) as left by the last run. */
+PCDM_API pcdm_status pcdm_residual(const pcdm_problem *p, float *r, void *stream);
+
+/* Philox4x32-10 of the library's device generator on `count` (ctr, key) pairs:
+ * ctr uint32[4*count], key uint32[2*count] -> out uint32[4*count]. */
+PCDM_API pcdm_status pcdm_philox(int64_t count, const uint32_t *ctr, const uint32_t *key, uint32_t *out,
+                        void *stream);
+
+/* Compares the library's device Philox with cuRAND's curand_Philox4x32_10 on
+ * `count` pseudo-random (ctr, key) pairs derived from `seed`; *mismatches = number
+ * of differing outputs. */
+PCDM_API pcdm_status pcdm_philox_check_curand(int64_t count, uint64_t seed, int64_t *mismatches,
+                                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCDM_H */

@@ -1,0 +1,84 @@
+// internal.h -- launch functions shared between the libpcdm translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pcdm_internal {
+
+struct DevCSC {
+    int64_t m, n, nnz;
+    const int64_t* colptr;  // device int64[n+1]
+    const int* rowidx;      // device int32[nnz]
+    const float* val;       // device float[nnz]
+};
+
+// ---- setup / occasional kernels (kernels_setup.cu)
+cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_check_finite(int64_t count, const float* v, int flag_bit, int* flags, cudaStream_t st,
+                                int sms, int64_t* launches);
+cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_max(int64_t count, const int* v, int* out, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
+                              cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,
+                           int64_t* launches);
+cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
+                                  cudaStream_t st, int sms, int64_t* launches);
+
+// ---- tau-nice sampler (kernels_sampler.cu)
+struct SamplerWork {
+    int64_t n, tau, cnt;        // cnt = slots drawn per iteration (tau or n - tau)
+    bool complement;            // 2 tau > n: draw the n - tau excluded values
+    int log2h;                  // hash table of 2^log2h uint64 entries per iteration
+    int64_t chunk;              // iterations per sampler pass
+    unsigned long long* tables; // [chunk][2^log2h]
+    int* cand;                  // [chunk][cnt] owned values (== slots when !complement)
+    int* pending;               // [chunk][cnt] pending slot lists
+    int* npending;              // [chunk]
+    unsigned char* marks;       // [chunk][n] (complement only)
+    int* rounds_max;            // device scalar
+};
+// Fill slots[it * tau + j] for it in [0, count), iterations k = k0 + it.
+cudaError_t sample_chunk(const SamplerWork& w, uint64_t seed, int64_t k0, int64_t count, int* slots,
+                         int* flags, cudaStream_t st, int sms, int64_t* launches);
+size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out);
+
+cudaError_t launch_philox(int64_t count, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
+                          cudaStream_t st);
+cudaError_t launch_philox_check_curand(int64_t count, uint64_t seed, unsigned long long* mismatches,
+                                       cudaStream_t st);
+
+// ---- iteration kernels (kernels_iter.cu)
+struct IterParams {
+    const int64_t* colptr;
+    const int* rowidx;
+    const float* val;
+    const float* L;
+    float* x;
+    float* r;
+    const int* slots;     // [iters][tau]
+    int64_t tau;
+    int64_t iters;
+    float beta;
+    float lambda;
+    int* nz_idx;          // [2][tau]
+    float* nz_delta;      // [2][tau]
+    int* nz_count;        // [2]
+    unsigned* barrier;    // zeroed before launch
+    int* flags;
+    unsigned long long* nz_total;  // accumulates #delta != 0
+    int64_t m, n;
+};
+
+struct IterLaunch {
+    int variant;          // pcdm_variant actually used
+    int ctas, threads, lanes;
+    size_t smem;
+};
+
+// Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
+IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device);
+cudaError_t launch_iter(const IterLaunch& L, const IterParams& P, cudaStream_t st, int64_t* launches);
+
+}  // namespace pcdm_internal

@@ -1,0 +1,236 @@
+// kernels_sampler.cu -- seeded tau-nice sampler on the device.
+//
+// Law: S_k uniform over all tau-subsets of [n] (tau-nice).
+// Concrete rule (reading R#1, SURVEY 8(c) "SAMPLE"): slot j of
+// iteration k draws, in rounds rho = 0, 1, ..., the Lemire-mapped Philox4x32-10
+// word of counter (j, k, rho, tag) under key (lo32 seed, hi32 seed); each value
+// is owned by the lexicographically smallest (rho, j) that drew it; unowned
+// slots redraw in the next round.  If 2 tau > n the n - tau EXCLUDED values are
+// drawn (tag 2) and S_k is the complement in ascending order.
+//
+// Device realisation: round 0 for every (iteration, slot) of a chunk is one
+// grid-wide pass inserting (value, code = rho*cnt + j) into a per-iteration
+// open-addressing table that keeps the minimum code per value (64-bit
+// atomicMin on (value << 32 | code)); a second pass keeps the owners; the few
+// leftover slots finish their rounds inside one CTA per iteration.  The result
+// depends only on the codes, never on thread timing.
+#include <cub/block/block_scan.cuh>
+#include <cuda_runtime.h>
+#include <curand_kernel.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace pcdm;
+
+namespace {
+
+struct DrawArgs {
+    uint64_t seed;
+    uint64_t n;
+    uint64_t reject_below;
+    uint32_t tag;
+    int64_t cnt;
+    int log2h;
+};
+
+__global__ void sample_round0_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables,
+                                     int* cand) {
+    const int64_t total = count * a.cnt;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t it = t / a.cnt;
+        const uint32_t j = (uint32_t)(t - it * a.cnt);
+        const long long v = draw_value(a.seed, (uint32_t)(k0 + it), 0u, j, a.tag, a.n, a.reject_below);
+        cand[t] = (int)v;
+        if (v >= 0) table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+    }
+}
+
+__global__ void sample_check_kernel(DrawArgs a, int64_t count, const unsigned long long* tables,
+                                    const int* cand, int* pending, int* npending) {
+    const int64_t total = count * a.cnt;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t it = t / a.cnt;
+        const uint32_t j = (uint32_t)(t - it * a.cnt);
+        const int v = cand[t];
+        const bool owned = v >= 0 && table_owner(tables + (it << a.log2h), a.log2h, (uint32_t)v) == j;
+        if (!owned) {
+            const int pos = atomicAdd(npending + it, 1);
+            pending[it * 2 * a.cnt + pos] = (int)j;
+        }
+    }
+}
+
+// One CTA per iteration finishes rounds rho >= 1 for its pending slots.
+__global__ void sample_rounds_kernel(DrawArgs a, int64_t k0, unsigned long long* tables, int* cand,
+                                     int* pending, const int* npending, int* rounds_max, int* flags) {
+    const int64_t it = blockIdx.x;
+    int np = npending[it];
+    if (np == 0) return;
+    unsigned long long* table = tables + (it << a.log2h);
+    int* c = cand + it * a.cnt;
+    int* pin = pending + it * 2 * a.cnt;
+    int* pout = pin + a.cnt;
+    __shared__ int s_next;
+    uint32_t rho = 1;
+    for (; np > 0; ++rho) {
+        if ((uint64_t)(rho + 1) * (uint64_t)a.cnt > 0x100000000ull) {
+            if (threadIdx.x == 0) atomicOr(flags, FLAG_SAMPLER);
+            return;
+        }
+        for (int t = threadIdx.x; t < np; t += blockDim.x) {
+            const uint32_t j = (uint32_t)pin[t];
+            const long long v = draw_value(a.seed, (uint32_t)(k0 + it), rho, j, a.tag, a.n, a.reject_below);
+            c[j] = (int)v;
+            if (v >= 0) table_insert(table, a.log2h, (uint32_t)v, rho * (uint32_t)a.cnt + j);
+        }
+        if (threadIdx.x == 0) s_next = 0;
+        __syncthreads();
+        for (int t = threadIdx.x; t < np; t += blockDim.x) {
+            const uint32_t j = (uint32_t)pin[t];
+            const int v = c[j];
+            const bool owned = v >= 0 && table_owner(table, a.log2h, (uint32_t)v) == rho * (uint32_t)a.cnt + j;
+            if (!owned) pout[atomicAdd(&s_next, 1)] = (int)j;
+        }
+        __syncthreads();
+        np = s_next;
+        int* tmp = pin;
+        pin = pout;
+        pout = tmp;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) atomicMax(rounds_max, (int)rho);
+}
+
+// Complement: S_k = [n] minus the owned (excluded) values, ascending.
+constexpr int kScanThreads = 512;
+__global__ void __launch_bounds__(kScanThreads) sample_complement_kernel(int64_t n, int64_t tau, int64_t cnt,
+                                                                         const int* cand, unsigned char* marks,
+                                                                         int* slots) {
+    using Scan = cub::BlockScan<int, kScanThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int s_base;
+    const int64_t it = blockIdx.x;
+    unsigned char* mk = marks + it * n;
+    const int* c = cand + it * cnt;
+    for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) mk[c[j]] = 1;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    int* out = slots + it * tau;
+    for (int64_t v0 = 0; v0 < n; v0 += kScanThreads) {
+        const int64_t v = v0 + threadIdx.x;
+        const int keep = (v < n && !mk[v]) ? 1 : 0;
+        int pos, total;
+        Scan(tmp).ExclusiveSum(keep, pos, total);
+        if (keep) out[s_base + pos] = (int)v;
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += total;
+        __syncthreads();
+    }
+}
+
+__global__ void philox_kernel(int64_t count, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        u32x4 c{ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], ctr[4 * t + 3]};
+        u32x4 o = philox4x32_10(c, key[2 * t], key[2 * t + 1]);
+        out[4 * t] = o.x;
+        out[4 * t + 1] = o.y;
+        out[4 * t + 2] = o.z;
+        out[4 * t + 3] = o.w;
+    }
+}
+
+__global__ void philox_curand_kernel(int64_t count, uint64_t seed, unsigned long long* mismatches) {
+    unsigned long long bad = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        // pseudo-random (ctr, key) derived from t and seed through our own generator
+        u32x4 h = philox4x32_10(u32x4{(uint32_t)t, (uint32_t)(t >> 32), 0x1234567u, 0x89abcdefu},
+                                (uint32_t)seed, (uint32_t)(seed >> 32));
+        u32x4 h2 = philox4x32_10(u32x4{h.w, h.z, h.y, h.x}, h.x, h.y);
+        const uint4 c4 = make_uint4(h.x, h.y, h.z, h.w);
+        const uint2 k2 = make_uint2(h2.x, h2.y);
+        const uint4 ref = curand_Philox4x32_10(c4, k2);
+        const u32x4 ours = philox4x32_10(u32x4{h.x, h.y, h.z, h.w}, h2.x, h2.y);
+        bad += (ref.x != ours.x) + (ref.y != ours.y) + (ref.z != ours.z) + (ref.w != ours.w);
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+inline int blocks_for(int64_t work, int threads, int max_blocks) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+}  // namespace
+
+namespace pcdm_internal {
+
+size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out) {
+    const bool comp = 2 * tau > n;
+    const int64_t cnt = comp ? n - tau : tau;
+    int log2h = 0;
+    while ((int64_t(1) << log2h) < 2 * cnt) ++log2h;
+    if (log2h_out) *log2h_out = log2h;
+    size_t bytes = ((size_t)1 << log2h) * 8 + (size_t)cnt * 4 * 2 + sizeof(int);
+    if (comp) bytes += (size_t)cnt * 4 + (size_t)n;
+    return bytes;
+}
+
+cudaError_t sample_chunk(const SamplerWork& w, uint64_t seed, int64_t k0, int64_t count, int* slots,
+                         int* flags, cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e;
+    DrawArgs a;
+    a.seed = seed;
+    a.n = (uint64_t)w.n;
+    a.reject_below = (uint64_t)(0 - (uint64_t)w.n) % (uint64_t)w.n;
+    a.tag = w.complement ? 2u : 1u;
+    a.cnt = w.cnt;
+    a.log2h = w.log2h;
+    int* cand = w.complement ? w.cand : slots;
+    if (w.cnt > 0) {
+        e = cudaMemsetAsync(w.tables, 0xFF, (size_t)count * ((size_t)1 << w.log2h) * 8, st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(w.npending, 0, (size_t)count * sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        const int blocks = blocks_for(count * w.cnt, 256, sms * 8);
+        sample_round0_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
+        sample_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
+        sample_rounds_kernel<<<(unsigned)count, 256, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
+                                                               w.rounds_max, flags);
+        *launches += 3;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (w.complement) {
+        e = cudaMemsetAsync(w.marks, 0, (size_t)count * (size_t)w.n, st);
+        if (e != cudaSuccess) return e;
+        sample_complement_kernel<<<(unsigned)count, kScanThreads, 0, st>>>(w.n, w.tau, w.cnt, w.cand, w.marks,
+                                                                          slots);
+        ++*launches;
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
+cudaError_t launch_philox(int64_t count, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
+                          cudaStream_t st) {
+    philox_kernel<<<blocks_for(count, 256, 4096), 256, 0, st>>>(count, ctr, key, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_philox_check_curand(int64_t count, uint64_t seed, unsigned long long* mismatches,
+                                       cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(mismatches, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    philox_curand_kernel<<<blocks_for(count, 256, 4096), 256, 0, st>>>(count, seed, mismatches);
+    return cudaGetLastError();
+}
+
+}  // namespace pcdm_internal

@@ -1,0 +1,246 @@
+// kernels_setup.cu -- create-time and occasional kernels of libpcdm:
+//   CSC validation, row histogram + omega, column norms
+//   L_i = ||a_i||^2, residual r = Ax - b (fp64 scratch), and
+//   the objective F = 1/2||r||^2 + lambda||x||_1 (eq:P).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace pcdm;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t work, int per_block, int max_blocks) {
+    int64_t b = (work + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+// One warp per column: colptr monotone, rows in [0,m) and strictly increasing,
+// values finite.
+__global__ void validate_kernel(int64_t m, int64_t n, int64_t nnz, const long long* __restrict__ colptr,
+                                const int* __restrict__ rowidx, const float* __restrict__ val,
+                                int* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int bad = 0;
+    if (warp == 0 && lane == 0) {
+        if (colptr[0] != 0 || colptr[n] != nnz) bad |= FLAG_BAD_COLPTR;
+    }
+    for (int64_t i = warp; i < n; i += nwarps) {
+        const long long s = colptr[i], e = colptr[i + 1];
+        if (e < s || s < 0 || e > nnz) {
+            bad |= FLAG_BAD_COLPTR;
+            continue;
+        }
+        for (long long p = s + lane; p < e; p += 32) {
+            const int r = rowidx[p];
+            if (r < 0 || (int64_t)r >= m) bad |= FLAG_BAD_ROW;
+            if (p > s && rowidx[p - 1] >= r) bad |= FLAG_ROW_ORDER;
+            if (!isfinite(val[p])) bad |= FLAG_NONFINITE_VAL;
+        }
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicOr(flags, bad);
+}
+
+__global__ void check_finite_kernel(int64_t count, const float* __restrict__ v, int flag_bit,
+                                    int* __restrict__ flags) {
+    int bad = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(v[t])) bad = flag_bit;
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, bad);
+}
+
+// counts[row]++ for every stored entry; warp-aggregated for hot rows.
+__global__ void row_counts_kernel(int64_t nnz, const int* __restrict__ rowidx, int* __restrict__ counts) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int r = ld_stream_s32(rowidx + p);
+        const unsigned active = __activemask();
+        const unsigned peers = __match_any_sync(active, r);
+        const int leader = __ffs(peers) - 1;
+        if ((threadIdx.x & 31) == leader) atomicAdd(counts + r, __popc(peers));
+    }
+}
+
+__global__ void max_kernel(int64_t count, const int* __restrict__ v, int* __restrict__ out) {
+    int best = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x)
+        best = max(best, v[t]);
+    best = __reduce_max_sync(0xffffffffu, best);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// L_i = sum_p val_p^2, fp64 accumulation, one warp per column (lanes stride).
+__global__ void col_norms_kernel(int64_t n, const long long* __restrict__ colptr,
+                                 const float* __restrict__ val, float* __restrict__ L) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        const long long s = colptr[i], e = colptr[i + 1];
+        double acc = 0.0;
+        for (long long p = s + lane; p < e; p += 32) {
+            const double v = (double)ld_stream_f32(val + p);
+            acc += v * v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) L[i] = (float)acc;
+    }
+}
+
+__global__ void neg_b_kernel(int64_t m, const float* __restrict__ b, double* __restrict__ r64) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+         t += (int64_t)gridDim.x * blockDim.x)
+        r64[t] = -(double)b[t];
+}
+
+// r64 += x_i a_i for x_i != 0 (thread per column; the support is small).  Also
+// flags non-finite x.
+__global__ void scatter_x_kernel(int64_t n, const long long* __restrict__ colptr,
+                                 const int* __restrict__ rowidx, const float* __restrict__ val,
+                                 const float* __restrict__ x, double* __restrict__ r64,
+                                 int* __restrict__ flags) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float xi = x[i];
+        if (xi == 0.0f) continue;
+        if (!isfinite(xi)) {
+            bad = FLAG_NONFINITE_X;
+            continue;
+        }
+        const double xd = (double)xi;
+        for (long long p = colptr[i]; p < colptr[i + 1]; ++p)
+            atomicAdd(r64 + rowidx[p], (double)val[p] * xd);
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, bad);
+}
+
+__global__ void round_r_kernel(int64_t m, const double* __restrict__ r64, float* __restrict__ r) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+         t += (int64_t)gridDim.x * blockDim.x)
+        r[t] = (float)r64[t];
+}
+
+// out[0] += sum r64^2 ; out[1] += sum |x|
+__global__ void objective_sums_kernel(int64_t m, int64_t n, const double* __restrict__ r64,
+                                      const float* __restrict__ x, double* __restrict__ out) {
+    double s2 = 0.0, s1 = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += stride)
+        s2 += r64[t] * r64[t];
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride)
+        s1 += fabs((double)x[t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    __shared__ double sh[2][32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sh[0][w] = s2;
+        sh[1][w] = s1;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        s2 = lane < nw ? sh[0][lane] : 0.0;
+        s1 = lane < nw ? sh[1][lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        if (lane == 0) {
+            atomicAdd(out, s2);
+            atomicAdd(out + 1, s1);
+        }
+    }
+}
+
+}  // namespace
+
+namespace pcdm_internal {
+
+cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches) {
+    const int blocks = grid_for(A.n * 32, kThreads, sms * 16);
+    validate_kernel<<<blocks, kThreads, 0, st>>>(A.m, A.n, A.nnz, (const long long*)A.colptr, A.rowidx,
+                                                 A.val, flags);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(int64_t count, const float* v, int flag_bit, int* flags, cudaStream_t st,
+                                int sms, int64_t* launches) {
+    const int blocks = grid_for(count, kThreads, sms * 8);
+    check_finite_kernel<<<blocks, kThreads, 0, st>>>(count, v, flag_bit, flags);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)A.m, st);
+    if (e != cudaSuccess) return e;
+    const int blocks = grid_for(A.nnz, kThreads, sms * 16);
+    row_counts_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, counts);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_max(int64_t count, const int* v, int* out, cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    const int blocks = grid_for(count, kThreads, sms * 8);
+    max_kernel<<<blocks, kThreads, 0, st>>>(count, v, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms, int64_t* launches) {
+    const int blocks = grid_for(A.n * 32, kThreads, sms * 16);
+    col_norms_kernel<<<blocks, kThreads, 0, st>>>(A.n, (const long long*)A.colptr, A.val, L);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
+                              cudaStream_t st, int sms, int64_t* launches) {
+    neg_b_kernel<<<grid_for(A.m, kThreads, sms * 8), kThreads, 0, st>>>(A.m, b, r64);
+    scatter_x_kernel<<<grid_for(A.n, kThreads, sms * 8), kThreads, 0, st>>>(
+        A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,
+                           int64_t* launches) {
+    round_r_kernel<<<grid_for(m, kThreads, sms * 8), kThreads, 0, st>>>(m, r64, r);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
+                                  cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    objective_sums_kernel<<<grid_for(m > n ? m : n, kThreads, sms * 4), kThreads, 0, st>>>(m, n, r64, x, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace pcdm_internal

@@ -1,0 +1,593 @@
+// pcdm_abi.cu -- host side of libpcdm.so: the C ABI declared in include/pcdm.h.
+//
+// Owns the problem handle (device copies of A, b, L, r, scratch), drives the
+// create-time kernels, and runs the PCDM1 loop as alternating sampler passes
+// and persistent iteration-kernel launches on the caller's stream.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/pcdm.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace pcdm_internal;
+
+namespace {
+
+thread_local std::string g_error = "no error";
+
+pcdm_status fail(pcdm_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    return s;
+}
+
+pcdm_status cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? PCDM_ENOMEM : PCDM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                  \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Scalars living in one small device block.
+struct Scalars {
+    int flags;
+    unsigned barrier;
+    int nz_count[2];
+    int max_out;
+    int rounds_max;
+    unsigned long long nz_total;
+    unsigned long long mismatches;
+    double sums[2];
+};
+
+}  // namespace
+
+struct pcdm_problem {
+    int device = 0;
+    int sms = 148;
+    int64_t m = 0, n = 0, nnz = 0;
+    double lambda = 0.0;
+    int64_t omega = 0;
+    int64_t* colptr = nullptr;
+    int* rowidx = nullptr;
+    float* val = nullptr;
+    float* b = nullptr;
+    float* L = nullptr;
+    float* r = nullptr;
+    double* r64 = nullptr;
+    float* xbuf = nullptr;     // device iterate when the caller passes host x
+    Scalars* sc = nullptr;     // device scalars
+    // per-run workspaces (grown on demand)
+    int* nz_idx = nullptr;
+    float* nz_delta = nullptr;
+    int64_t nz_cap = 0;
+    void* samp_mem = nullptr;
+    size_t samp_cap = 0;
+    pcdm_run_stats stats{};
+    std::vector<cudaEvent_t> events;  // timing events, reused across runs
+    DevCSC csc() const { return DevCSC{m, n, nnz, colptr, rowidx, val}; }
+};
+
+namespace {
+
+template <typename T>
+pcdm_status dev_copy_in(T** dst, const T* src, size_t count, cudaStream_t st, const char* what) {
+    CK(cudaMalloc((void**)dst, sizeof(T) * (count ? count : 1)), what);
+    if (count) CK(cudaMemcpyAsync(*dst, src, sizeof(T) * count, cudaMemcpyDefault, st), what);
+    return PCDM_OK;
+}
+
+void free_problem(pcdm_problem* p) {
+    if (!p) return;
+    cudaFree(p->colptr);
+    cudaFree(p->rowidx);
+    cudaFree(p->val);
+    cudaFree(p->b);
+    cudaFree(p->L);
+    cudaFree(p->r);
+    cudaFree(p->r64);
+    cudaFree(p->xbuf);
+    cudaFree(p->sc);
+    cudaFree(p->nz_idx);
+    cudaFree(p->nz_delta);
+    cudaFree(p->samp_mem);
+    for (cudaEvent_t e : p->events) cudaEventDestroy(e);
+    delete p;
+}
+
+const char* flag_text(int f) {
+    if (f & FLAG_BAD_COLPTR) return "colptr must start at 0, end at nnz and be non-decreasing";
+    if (f & FLAG_BAD_ROW) return "row index out of [0, m)";
+    if (f & FLAG_ROW_ORDER) return "row indices must be strictly increasing within each column";
+    if (f & FLAG_NONFINITE_VAL) return "non-finite value in val";
+    if (f & FLAG_NONFINITE_B) return "non-finite value in b";
+    if (f & FLAG_NONFINITE_X) return "non-finite value in x";
+    return "invalid input";
+}
+
+pcdm_status read_scalars(pcdm_problem* p, Scalars* host, cudaStream_t st) {
+    CK(cudaMemcpyAsync(host, p->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st), "read scalars");
+    CK(cudaStreamSynchronize(st), "stream synchronize");
+    return PCDM_OK;
+}
+
+// r <- A x - b with fp64 accumulation (x device pointer).
+pcdm_status residual_from(pcdm_problem* p, const float* x, cudaStream_t st, int64_t* launches) {
+    CK(launch_residual64(p->csc(), p->b, x, p->r64, &p->sc->flags, st, p->sms, launches), "residual kernels");
+    CK(launch_round_r(p->m, p->r64, p->r, st, p->sms, launches), "residual rounding");
+    return PCDM_OK;
+}
+
+// Device-time accounting of a run: event pairs recorded on the run's stream
+// around each phase; summed after the final synchronisation.
+struct RunTimer {
+    pcdm_problem* p;
+    cudaStream_t st;
+    std::vector<std::pair<int, int>> marks;  // (kind, index of the start event)
+    int used = 0;
+    cudaError_t record(int* idx) {
+        if ((int)p->events.size() <= used) {
+            cudaEvent_t e;
+            cudaError_t err = cudaEventCreate(&e);
+            if (err != cudaSuccess) return err;
+            p->events.push_back(e);
+        }
+        *idx = used++;
+        return cudaEventRecord(p->events[*idx], st);
+    }
+    cudaError_t begin(int* idx) { return record(idx); }
+    cudaError_t end(int kind, int start_idx) {
+        int e;
+        cudaError_t err = record(&e);
+        marks.push_back({kind, start_idx});
+        return err;
+    }
+    void sum(double out[3]) {
+        out[0] = out[1] = out[2] = 0.0;
+        for (auto& mk : marks) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, p->events[mk.second], p->events[mk.second + 1]) == cudaSuccess)
+                out[mk.first] += ms;
+        }
+        cudaGetLastError();
+    }
+};
+enum { T_ITER = 0, T_SAMPLER = 1, T_SETUP = 2 };
+
+int64_t refresh_period(int64_t n, int64_t tau, int64_t refresh_every) {
+    if (refresh_every < 0) return 0;
+    if (refresh_every > 0) return refresh_every;
+    return (2 * n + tau - 1) / tau;
+}
+
+struct SamplerPlan {
+    SamplerWork w;
+    int* slots;
+};
+
+// Carve the sampler + slot workspace for `chunk` iterations out of p->samp_mem.
+pcdm_status sampler_workspace(void** mem, size_t* cap, int64_t n, int64_t tau, int64_t chunk, SamplerPlan* sp) {
+    int log2h = 0;
+    sampler_bytes_per_iter(n, tau, &log2h);
+    const bool comp = 2 * tau > n;
+    const int64_t cnt = comp ? n - tau : tau;
+    auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+    size_t off = 0;
+    const size_t o_tables = off; off += al((size_t)chunk * ((size_t)1 << log2h) * 8);
+    const size_t o_slots = off; off += al((size_t)chunk * tau * 4);
+    const size_t o_cand = off; off += comp ? al((size_t)chunk * cnt * 4) : 0;
+    const size_t o_pend = off; off += al((size_t)chunk * 2 * (cnt ? cnt : 1) * 4);
+    const size_t o_np = off; off += al((size_t)chunk * 4);
+    const size_t o_marks = off; off += comp ? al((size_t)chunk * n) : 0;
+    const size_t o_rmax = off; off += 256;
+    if (off > *cap) {
+        cudaFree(*mem);
+        *mem = nullptr;
+        *cap = 0;
+        CK(cudaMalloc(mem, off), "sampler workspace");
+        *cap = off;
+    }
+    char* base = (char*)*mem;
+    sp->w.n = n;
+    sp->w.tau = tau;
+    sp->w.cnt = cnt;
+    sp->w.complement = comp;
+    sp->w.log2h = log2h;
+    sp->w.chunk = chunk;
+    sp->w.tables = (unsigned long long*)(base + o_tables);
+    sp->w.cand = comp ? (int*)(base + o_cand) : nullptr;
+    sp->w.pending = (int*)(base + o_pend);
+    sp->w.npending = (int*)(base + o_np);
+    sp->w.marks = comp ? (unsigned char*)(base + o_marks) : nullptr;
+    sp->w.rounds_max = (int*)(base + o_rmax);
+    sp->slots = (int*)(base + o_slots);
+    return PCDM_OK;
+}
+
+int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
+    const size_t per = sampler_bytes_per_iter(n, tau, nullptr) + (size_t)tau * 4;
+    const size_t budget = (size_t)512 << 20;
+    int64_t c = (int64_t)std::max<size_t>(1, budget / per);
+    c = std::min<int64_t>(c, 8192);
+    return std::min<int64_t>(c, std::max<int64_t>(iters, 1));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pcdm_last_error(void) { return g_error.c_str(); }
+
+pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
+                        const float* val, const float* b, double lambda, void* stream, pcdm_problem** out) {
+    if (!out) return fail(PCDM_EINVAL, "out must not be NULL");
+    *out = nullptr;
+    if (m < 1 || n < 1 || nnz < 1) return fail(PCDM_EINVAL, "need m, n, nnz >= 1 (no loss terms otherwise)");
+    if (m >= (1ll << 31) || n >= (1ll << 31)) return fail(PCDM_EINVAL, "m and n must be < 2^31");
+    if (!colptr || !rowidx || !val || !b) return fail(PCDM_EINVAL, "NULL array argument");
+    if (!(lambda >= 0.0) || lambda > 1e308) return fail(PCDM_EINVAL, "lambda must be finite and >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    pcdm_problem* p = new pcdm_problem();
+    p->m = m;
+    p->n = n;
+    p->nnz = nnz;
+    p->lambda = lambda;
+    pcdm_status s = PCDM_OK;
+    int64_t launches = 0;
+    Scalars hs{};
+    do {
+        if (cudaGetDevice(&p->device) != cudaSuccess) { s = cuda_fail(cudaGetLastError(), "cudaGetDevice"); break; }
+        cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
+        if ((s = dev_copy_in(&p->colptr, colptr, (size_t)n + 1, st, "copy colptr")) != PCDM_OK) break;
+        if ((s = dev_copy_in(&p->rowidx, rowidx, (size_t)nnz, st, "copy rowidx")) != PCDM_OK) break;
+        if ((s = dev_copy_in(&p->val, val, (size_t)nnz, st, "copy val")) != PCDM_OK) break;
+        if ((s = dev_copy_in(&p->b, b, (size_t)m, st, "copy b")) != PCDM_OK) break;
+        cudaError_t e;
+        if ((e = cudaMalloc((void**)&p->sc, sizeof(Scalars))) != cudaSuccess) { s = cuda_fail(e, "scalars"); break; }
+        if ((e = cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st)) != cudaSuccess) { s = cuda_fail(e, "memset"); break; }
+        if ((e = launch_validate(p->csc(), &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "validate"); break; }
+        if ((e = launch_check_finite(m, p->b, FLAG_NONFINITE_B, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "check b"); break; }
+        if ((s = read_scalars(p, &hs, st)) != PCDM_OK) break;
+        if (hs.flags) { s = fail(PCDM_EINVAL, "invalid CSC input: %s", flag_text(hs.flags)); break; }
+        if ((e = cudaMalloc((void**)&p->L, sizeof(float) * n)) != cudaSuccess) { s = cuda_fail(e, "alloc L"); break; }
+        if ((e = launch_col_norms(p->csc(), p->L, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "col norms"); break; }
+        int* counts = nullptr;
+        if ((e = cudaMalloc((void**)&counts, sizeof(int) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc counts"); break; }
+        e = launch_row_counts(p->csc(), counts, st, p->sms, &launches);
+        if (e == cudaSuccess) e = launch_max(m, counts, &p->sc->max_out, st, p->sms, &launches);
+        if (e != cudaSuccess) { cudaFree(counts); s = cuda_fail(e, "row histogram"); break; }
+        s = read_scalars(p, &hs, st);
+        cudaFree(counts);
+        if (s != PCDM_OK) break;
+        p->omega = hs.max_out;
+        if ((e = cudaMalloc((void**)&p->r, sizeof(float) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc r"); break; }
+        if ((e = cudaMalloc((void**)&p->r64, sizeof(double) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc r64"); break; }
+        if ((e = cudaMemsetAsync(p->r, 0, sizeof(float) * m, st)) != cudaSuccess) { s = cuda_fail(e, "memset r"); break; }
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { s = cuda_fail(e, "create sync"); break; }
+    } while (0);
+    if (s != PCDM_OK) {
+        free_problem(p);
+        return s;
+    }
+    p->stats.kernel_launches = launches;
+    *out = p;
+    return PCDM_OK;
+}
+
+void pcdm_destroy(pcdm_problem* p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();
+    free_problem(p);
+}
+
+pcdm_status pcdm_omega(const pcdm_problem* p, int64_t* omega) {
+    if (!p || !omega) return fail(PCDM_EINVAL, "NULL argument");
+    *omega = p->omega;
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_beta(const pcdm_problem* p, int64_t tau, double* beta) {
+    if (!p || !beta) return fail(PCDM_EINVAL, "NULL argument");
+    if (tau < 1 || tau > p->n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
+    const double denom = (double)std::max<int64_t>(1, p->n - 1);
+    *beta = 1.0 + (double)(p->omega - 1) * (double)(tau - 1) / denom;
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_run(pcdm_problem* p, float* x, int64_t tau, int64_t iters, uint64_t seed, void* stream) {
+    return pcdm_run_ex(p, x, tau, iters, seed, 0, 0, 0.0, PCDM_VARIANT_AUTO, stream);
+}
+
+pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, uint64_t seed, int64_t first_iter,
+                        int64_t refresh_every, double beta_override, int32_t variant, void* stream) {
+    if (!p || !x) return fail(PCDM_EINVAL, "NULL argument");
+    if (tau < 1 || tau > p->n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
+    if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
+    if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
+    if (variant < 0 || variant > 3) return fail(PCDM_EINVAL, "unknown variant %d", variant);
+    if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
+    CK(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    pcdm_run_stats stats{};
+    int64_t launches = 0;
+
+    RunTimer tm{p, st};
+    int t0;
+    CK(tm.begin(&t0), "event");
+    // iterate buffer: device x in place, host x through xbuf
+    const bool x_dev = is_device_ptr(x);
+    float* xd = x;
+    if (!x_dev) {
+        if (!p->xbuf) CK(cudaMalloc((void**)&p->xbuf, sizeof(float) * p->n), "alloc x buffer");
+        CK(cudaMemcpyAsync(p->xbuf, x, sizeof(float) * p->n, cudaMemcpyHostToDevice, st), "copy x in");
+        xd = p->xbuf;
+    }
+    CK(cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st), "memset scalars");
+    pcdm_status s = residual_from(p, xd, st, &launches);
+    if (s != PCDM_OK) return s;
+    CK(tm.end(T_SETUP, t0), "event");
+    Scalars hs{};
+    if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
+    if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
+
+    double beta_d;
+    pcdm_beta(p, tau, &beta_d);
+    if (beta_override > 0.0) beta_d = beta_override;
+    const int64_t R = refresh_period(p->n, tau, refresh_every);
+    const IterLaunch plan = plan_iter(variant, p->m, p->n, p->nnz, tau, p->sms, p->device);
+    if (p->nz_cap < tau) {
+        cudaFree(p->nz_idx);
+        cudaFree(p->nz_delta);
+        p->nz_idx = nullptr;
+        p->nz_delta = nullptr;
+        p->nz_cap = 0;
+        CK(cudaMalloc((void**)&p->nz_idx, sizeof(int) * 2 * tau), "alloc step list");
+        CK(cudaMalloc((void**)&p->nz_delta, sizeof(float) * 2 * tau), "alloc step list");
+        p->nz_cap = tau;
+    }
+    int64_t chunk = choose_chunk(p->n, tau, iters);
+    if (R > 0) chunk = std::min(chunk, R);
+    SamplerPlan sp;
+    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, chunk, &sp)) != PCDM_OK) return s;
+    CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), st), "memset rounds");
+
+    IterParams P{};
+    P.colptr = p->colptr;
+    P.rowidx = p->rowidx;
+    P.val = p->val;
+    P.L = p->L;
+    P.x = xd;
+    P.r = p->r;
+    P.tau = tau;
+    P.beta = (float)beta_d;
+    P.lambda = (float)p->lambda;
+    P.nz_idx = p->nz_idx;
+    P.nz_delta = p->nz_delta;
+    P.nz_count = p->sc->nz_count;
+    P.barrier = &p->sc->barrier;
+    P.flags = &p->sc->flags;
+    P.nz_total = &p->sc->nz_total;
+    P.m = p->m;
+    P.n = p->n;
+
+    int64_t done = 0;
+    while (done < iters) {
+        int64_t c = std::min(chunk, iters - done);
+        if (R > 0) c = std::min(c, R - (done % R));
+        int ts;
+        CK(tm.begin(&ts), "event");
+        CK(sample_chunk(sp.w, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
+           "sampler");
+        // zero barrier counter and both step-list counters (contiguous in Scalars)
+        CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + 2 * sizeof(int), st), "memset barrier");
+        CK(tm.end(T_SAMPLER, ts), "event");
+        P.slots = sp.slots;
+        P.iters = c;
+        int ti;
+        CK(tm.begin(&ti), "event");
+        CK(launch_iter(plan, P, st, &launches), "iteration kernel");
+        CK(tm.end(T_ITER, ti), "event");
+        ++stats.iter_launches;
+        done += c;
+        if (R > 0 && done % R == 0) {
+            int tr;
+            CK(tm.begin(&tr), "event");
+            if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) return s;
+            CK(tm.end(T_SETUP, tr), "event");
+            ++stats.refreshes;
+        }
+    }
+    int tx;
+    CK(tm.begin(&tx), "event");
+    if (!x_dev) CK(cudaMemcpyAsync(x, p->xbuf, sizeof(float) * p->n, cudaMemcpyDeviceToHost, st), "copy x out");
+    CK(tm.end(T_SETUP, tx), "event");
+    int rmax = 0;
+    CK(cudaMemcpyAsync(&rmax, sp.w.rounds_max, sizeof(int), cudaMemcpyDeviceToHost, st), "read rounds");
+    if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
+
+    stats.iters = iters;
+    stats.nonzero_deltas = (int64_t)hs.nz_total;
+    stats.sampler_max_rounds = iters > 0 ? std::max(1, rmax) : 0;
+    stats.kernel_launches = launches;
+    stats.variant = plan.variant;
+    stats.grid_ctas = plan.ctas;
+    stats.threads_per_cta = plan.threads;
+    stats.lanes_per_column = plan.lanes;
+    stats.chunk_iters = chunk;
+    double tms[3];
+    tm.sum(tms);
+    stats.iter_kernel_ms = tms[T_ITER];
+    stats.sampler_ms = tms[T_SAMPLER];
+    stats.setup_ms = tms[T_SETUP];
+    p->stats = stats;
+    if (hs.flags & FLAG_SAMPLER) return fail(PCDM_ESAMPLER, "sampler round counter overflow");
+    if (hs.flags & FLAG_DIVERGED) return fail(PCDM_EDIVERGED, "non-finite step (diverged)");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_objective(pcdm_problem* p, const float* x, double* F, void* stream) {
+    if (!p || !x || !F) return fail(PCDM_EINVAL, "NULL argument");
+    CK(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t launches = 0;
+    const float* xd = x;
+    float* tmp = nullptr;
+    if (!is_device_ptr(x)) {
+        CK(cudaMalloc((void**)&tmp, sizeof(float) * p->n), "alloc x");
+        CK(cudaMemcpyAsync(tmp, x, sizeof(float) * p->n, cudaMemcpyHostToDevice, st), "copy x");
+        xd = tmp;
+    }
+    pcdm_status s = PCDM_OK;
+    Scalars hs{};
+    do {
+        cudaError_t e = cudaMemsetAsync(&p->sc->flags, 0, sizeof(int), st);
+        if (e != cudaSuccess) { s = cuda_fail(e, "memset"); break; }
+        if ((e = launch_residual64(p->csc(), p->b, xd, p->r64, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "residual"); break; }
+        if ((e = launch_objective_sums(p->m, p->n, p->r64, xd, p->sc->sums, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "objective"); break; }
+        s = read_scalars(p, &hs, st);
+    } while (0);
+    cudaFree(tmp);
+    if (s != PCDM_OK) return s;
+    if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
+    *F = 0.5 * hs.sums[0] + p->lambda * hs.sums[1];
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_last_run_stats(const pcdm_problem* p, pcdm_run_stats* stats) {
+    if (!p || !stats) return fail(PCDM_EINVAL, "NULL argument");
+    *stats = p->stats;
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_sample(int64_t n, int64_t tau, uint64_t seed, int64_t first_iter, int64_t count, int32_t* slots,
+                        void* stream) {
+    if (!slots) return fail(PCDM_EINVAL, "NULL argument");
+    if (n < 1 || n >= (1ll << 31)) return fail(PCDM_EINVAL, "n must be in [1, 2^31)");
+    if (tau < 1 || tau > n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
+    if (count < 0 || first_iter < 0 || first_iter + count > (1ll << 32))
+        return fail(PCDM_EINVAL, "bad iteration range");
+    if (count == 0) return PCDM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t chunk = choose_chunk(n, tau, count);
+    void* mem = nullptr;
+    size_t cap = 0;
+    int* flags = nullptr;
+    SamplerPlan sp;
+    pcdm_status s = sampler_workspace(&mem, &cap, n, tau, chunk, &sp);
+    if (s != PCDM_OK) return s;
+    int64_t launches = 0;
+    cudaError_t e = cudaMalloc((void**)&flags, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(int), st);
+    const bool dev_out = is_device_ptr(slots);
+    for (int64_t done = 0; e == cudaSuccess && done < count;) {
+        const int64_t c = std::min(chunk, count - done);
+        e = sample_chunk(sp.w, seed, first_iter + done, c, sp.slots, flags, st, sms, &launches);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(slots + done * tau, sp.slots, sizeof(int) * c * tau,
+                                dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st);
+        done += c;
+    }
+    int hflags = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(mem);
+    cudaFree(flags);
+    if (e != cudaSuccess) return cuda_fail(e, "pcdm_sample");
+    if (hflags & FLAG_SAMPLER) return fail(PCDM_ESAMPLER, "sampler round counter overflow");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_col_norms(const pcdm_problem* p, float* L, void* stream) {
+    if (!p || !L) return fail(PCDM_EINVAL, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(L, p->L, sizeof(float) * p->n, cudaMemcpyDefault, st), "copy L");
+    CK(cudaStreamSynchronize(st), "sync");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_row_counts(const pcdm_problem* p, int32_t* counts, void* stream) {
+    if (!p || !counts) return fail(PCDM_EINVAL, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t launches = 0;
+    int* d = nullptr;
+    CK(cudaMalloc((void**)&d, sizeof(int) * p->m), "alloc counts");
+    cudaError_t e = launch_row_counts(p->csc(), d, st, p->sms, &launches);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(counts, d, sizeof(int) * p->m, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "row counts");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_residual(const pcdm_problem* p, float* r, void* stream) {
+    if (!p || !r) return fail(PCDM_EINVAL, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(r, p->r, sizeof(float) * p->m, cudaMemcpyDefault, st), "copy r");
+    CK(cudaStreamSynchronize(st), "sync");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_philox(int64_t count, const uint32_t* ctr, const uint32_t* key, uint32_t* out, void* stream) {
+    if (count < 0 || (count > 0 && (!ctr || !key || !out))) return fail(PCDM_EINVAL, "bad arguments");
+    if (count == 0) return PCDM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *dc = nullptr, *dk = nullptr, *dout = nullptr;
+    cudaError_t e = cudaMalloc((void**)&dc, 16 * count);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dk, 8 * count);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dout, 16 * count);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dc, ctr, 16 * count, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dk, key, 8 * count, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = launch_philox(count, dc, dk, dout, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, 16 * count, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dc);
+    cudaFree(dk);
+    cudaFree(dout);
+    if (e != cudaSuccess) return cuda_fail(e, "pcdm_philox");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_philox_check_curand(int64_t count, uint64_t seed, int64_t* mismatches, void* stream) {
+    if (!mismatches || count < 0) return fail(PCDM_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d = nullptr;
+    unsigned long long h = 0;
+    cudaError_t e = cudaMalloc((void**)&d, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = launch_philox_check_curand(count, seed, d, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "pcdm_philox_check_curand");
+    *mismatches = (int64_t)h;
+    return PCDM_OK;
+}
+
+}  // extern "C"

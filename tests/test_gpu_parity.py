@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bit-exact: Philox words, sampled slot arrays, omega, row histogram.
+Tolerance (north_star, BASELINE.json): F within 1e-5 relative, ||dx||_inf <=
+1e-4 ||x||_inf; L_i within fp32 rounding of the oracle's fp64 value.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import ref_sampler
+from paper_1212_0873_b200 import instances as I
+from paper_1212_0873_b200 import pcdm
+from parity_util import assert_parity, run_both, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------------ Philox / sampler
+def test_philox_matches_oracle_and_curand(gpu):
+    rng = np.random.default_rng(0)
+    N = 4096
+    ctr = rng.integers(0, 1 << 32, size=4 * N, dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 1 << 32, size=2 * N, dtype=np.uint64).astype(np.uint32)
+    out = np.zeros(4 * N, dtype=np.uint32)
+    pcdm.pcdm_philox(ctr, key, out, stream=0)
+    for t in range(0, N, 97):
+        assert list(out[4 * t:4 * t + 4]) == list(oracle.philox4x32_10(ctr[4 * t:4 * t + 4], key[2 * t:2 * t + 2]))
+    # P1: the device generator against cuRAND's curand_Philox4x32_10 on 1e6 pairs
+    assert pcdm.pcdm_philox_check_curand(1 << 20, 12345) == 0
+
+
+@pytest.mark.parametrize("n,tau,count", [
+    (1, 1, 3), (2, 1, 5), (2, 2, 2), (5, 2, 50), (7, 5, 50), (20, 8, 50), (20, 15, 30),
+    (100, 50, 20), (100, 51, 20), (97, 96, 10), (64, 64, 3), (1000, 32, 200),
+    (100_000, 1024, 100), (3000, 1400, 5)])
+def test_sampler_bitexact_small(gpu, n, tau, count):
+    for seed in (0, 7):
+        for first in (0, 1000):
+            got = np.zeros(count * tau, dtype=np.int32)
+            pcdm.pcdm_sample(n, tau, seed, first, count, got, stream=0)
+            got = got.reshape(count, tau)
+            for k in range(count):
+                want = oracle.sample(seed, first + k, tau, n)
+                assert np.array_equal(got[k], want), (seed, first + k)
+            if n * count <= 4000:
+                assert list(got[0]) == ref_sampler.sample(seed, first, tau, n)
+
+
+@pytest.mark.parametrize("cfg,tau,count", [("skewed", 1 << 16, 12), ("skewed", 1 << 8, 50),
+                                           ("large", 65536, 8), ("huge", 1 << 18, 3)])
+def test_sampler_bitexact_config_shapes(gpu, cfg, tau, count):
+    n = I.CONFIGS[cfg].n
+    got = torch.zeros(count * tau, dtype=torch.int32, device=gpu)
+    pcdm.pcdm_sample(n, tau, 0, 0, count, got)
+    got = to_host(got).reshape(count, tau)
+    for k in range(count):
+        assert np.array_equal(got[k], oracle.sample(0, k, tau, n)), k
+
+
+def test_sampler_high_collision_rounds(gpu):
+    # tau close to n/2 forces many ownership rounds; still bit-exact
+    n, tau, count = 4001, 2000, 6
+    got = np.zeros(count * tau, dtype=np.int32)
+    pcdm.pcdm_sample(n, tau, 3, 0, count, got, stream=0)
+    for k in range(count):
+        assert np.array_equal(got[k * tau:(k + 1) * tau], oracle.sample(3, k, tau, n))
+
+
+# ------------------------------------------------------------------ omega, L, histogram
+@pytest.mark.parametrize("cfg", ["tiny", "medium", "skewed"])
+def test_omega_L_counts(gpu, cfg):
+    inst = I.generate(cfg, seed=0, device=gpu)
+    prob = pcdm.Problem.from_instance(inst)
+    c, r, v, b = inst.numpy()
+    assert prob.omega == oracle.omega(inst.m, r)
+    counts = torch.zeros(inst.m, dtype=torch.int32, device=gpu)
+    prob.row_counts(counts)
+    assert np.array_equal(to_host(counts), oracle.row_counts(inst.m, r))
+    L = torch.zeros(inst.n, dtype=torch.float32, device=gpu)
+    prob.col_norms(L)
+    Lo = oracle.col_norms(c, v).astype(np.float32)  # fp64 value rounded to fp32
+    np.testing.assert_allclose(to_host(L), Lo, rtol=2e-7, atol=0)
+    prob.close()
+
+
+# ------------------------------------------------------------------ full runs
+@pytest.mark.parametrize("variant", ["auto", "smem", "block", "grid"])
+def test_tiny_config_full_run(gpu, variant):
+    # BASELINE configs[0]: tiny, tau = 32, 2000 iterations, seed 0
+    inst = I.generate("tiny", seed=0)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 32, 2000, seed=0,
+                   variant=variant)
+    assert_parity(out)
+    assert out["stats"]["iters"] == 2000
+    assert out["F_orc"] < 0.5 * float((inst.b.double() ** 2).sum())
+
+
+def test_medium_config_full_run(gpu):
+    inst = I.generate("medium", seed=0)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 1024, 10_000, seed=0)
+    assert_parity(out)
+    assert out["stats"]["variant"] == pcdm.VARIANTS["grid"]
+
+
+@pytest.mark.parametrize("tau", [1 << 8, 1 << 12, 1 << 16])
+def test_skewed_config(gpu, tau):
+    inst = I.generate("skewed", seed=0)
+    iters = {1 << 8: 3000, 1 << 12: 1000, 1 << 16: 100}[tau]
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, tau, iters, seed=0)
+    assert_parity(out)
+
+
+def test_large_config_reduced_iters(gpu):
+    inst = I.generate("large", seed=0, device=gpu)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 65536, 40, seed=0)
+    assert_parity(out)
+
+
+# ------------------------------------------------------------------ edge cases
+def _ragged(m, n, lens, seed, lam_frac=0.1):
+    colptr, rowidx, val = I.random_csc(m, n, lens, seed=seed)
+    b = I.random_b(m, seed=seed)
+    return colptr, rowidx, val, b, I.lam_for(colptr, rowidx, val, b, lam_frac)
+
+
+@pytest.mark.parametrize("variant", ["smem", "block", "grid"])
+def test_ragged_columns_with_empty_and_long(gpu, variant):
+    m, n = 3000, 700
+    rng = np.random.default_rng(1)
+    lens = rng.integers(0, 40, size=n)
+    lens[:7] = 0
+    lens[10] = 2999
+    lens[11] = 700
+    c, r, v, b, lam = _ragged(m, n, lens, 4)
+    for tau in (1, 7, 300, 699, 700):
+        out = run_both(c, r, v, b, lam, m, tau, 60, seed=tau, variant=variant,
+                       x0=np.random.default_rng(2).normal(size=n) * (np.arange(n) % 5 == 0))
+        assert_parity(out)
+
+
+@pytest.mark.parametrize("variant", ["smem", "grid"])
+def test_lambda_zero_and_beta_override(gpu, variant):
+    c, r, v, b, lam = _ragged(400, 300, np.full(300, 6), 9)
+    assert_parity(run_both(c, r, v, b, 0.0, 400, 16, 300, seed=1, variant=variant))
+    assert_parity(run_both(c, r, v, b, lam, 400, 16, 300, seed=1, beta_override=3.5, variant=variant))
+
+
+def test_resume_continues_the_stream(gpu):
+    c, r, v, b, lam = _ragged(2000, 1500, np.full(1500, 8), 5)
+    dev = gpu
+    prob = pcdm.Problem(2000, 1500, c.to(dev), r.to(dev), v.to(dev), b.to(dev), lam)
+    x1 = torch.zeros(1500, device=dev)
+    prob.run(x1, 64, 300, seed=11, refresh_every=-1)
+    x2 = torch.zeros(1500, device=dev)
+    prob.run(x2, 64, 120, seed=11, refresh_every=-1)
+    prob.run(x2, 64, 180, seed=11, first_iter=120, refresh_every=-1)
+    xo = oracle.run(2000, to_host(c), to_host(r), to_host(v), to_host(b), lam, 64, 300, 11,
+                    refresh_every=-1).x
+    for x in (x1, x2):
+        assert np.max(np.abs(to_host(x) - xo)) <= 1e-4 * np.max(np.abs(xo))
+    prob.close()
+
+
+def test_host_and_device_x_agree(gpu):
+    inst = I.generate("tiny", seed=3)
+    prob = pcdm.Problem.from_instance(inst.to(gpu))
+    xh = np.zeros(inst.n, dtype=np.float32)
+    xd = torch.zeros(inst.n, dtype=torch.float32, device=gpu)
+    prob.run(xh, 32, 500, seed=2, variant="grid")
+    prob.run(xd, 32, 500, seed=2, variant="grid")
+    np.testing.assert_allclose(xh, to_host(xd), rtol=1e-5, atol=1e-6)
+    assert abs(prob.objective(xh) - prob.objective(xd)) <= 1e-6 * prob.objective(xd)
+    prob.close()
+
+
+@pytest.mark.parametrize("refresh", [-1, 1, 7])
+def test_refresh_cadence(gpu, refresh):
+    c, r, v, b, lam = _ragged(500, 400, np.full(400, 5), 6)
+    out = run_both(c, r, v, b, lam, 500, 40, 100, seed=4, refresh_every=refresh, variant="grid")
+    assert_parity(out)
+    # maintained residual vs the oracle's (and vs Ax-b of the oracle's x)
+    np.testing.assert_allclose(out["r_gpu"], out["res"].r, rtol=0, atol=1e-4 * np.max(np.abs(out["res"].r)))
+
+
+def test_objective_matches_oracle(gpu):
+    inst = I.generate("medium", seed=1)
+    x = torch.randn(inst.n, generator=torch.Generator().manual_seed(0)) * (torch.rand(inst.n) < 0.05)
+    prob = pcdm.Problem.from_instance(inst.to(gpu))
+    F = prob.objective(x.to(gpu))
+    c, r, v, b = inst.numpy()
+    Fo = oracle.objective(inst.m, c, r, v, b, inst.lam, x.numpy().astype(np.float64))
+    assert abs(F - Fo) <= 1e-12 * abs(Fo)
+    prob.close()
+
+
+# ------------------------------------------------------------------ errors
+def test_errors(gpu):
+    c, r, v, b, lam = _ragged(50, 40, np.full(40, 3), 1)
+    dev = gpu
+    bad_r = r.clone()
+    bad_r[5] = 50
+    with pytest.raises(pcdm.PCDMError) as e:
+        pcdm.Problem(50, 40, c.to(dev), bad_r.to(dev), v.to(dev), b.to(dev), lam)
+    assert e.value.status == pcdm.PCDM_EINVAL and "row index" in e.value.message
+    unsorted = r.clone()
+    unsorted[0], unsorted[1] = r[1], r[0]
+    with pytest.raises(pcdm.PCDMError) as e:
+        pcdm.Problem(50, 40, c.to(dev), unsorted.to(dev), v.to(dev), b.to(dev), lam)
+    assert "strictly increasing" in e.value.message
+    bad_c = c.clone()
+    bad_c[-1] += 1
+    with pytest.raises(pcdm.PCDMError):
+        pcdm.Problem(50, 40, bad_c.to(dev), r.to(dev), v.to(dev), b.to(dev), lam)
+    nan_v = v.clone()
+    nan_v[3] = float("nan")
+    with pytest.raises(pcdm.PCDMError) as e:
+        pcdm.Problem(50, 40, c.to(dev), r.to(dev), nan_v.to(dev), b.to(dev), lam)
+    assert "val" in e.value.message
+    prob = pcdm.Problem(50, 40, c.to(dev), r.to(dev), v.to(dev), b.to(dev), lam)
+    x = torch.zeros(40, device=dev)
+    for tau in (0, 41):
+        with pytest.raises(pcdm.PCDMError) as e:
+            prob.run(x, tau, 1)
+        assert e.value.status == pcdm.PCDM_EINVAL
+    x[3] = float("inf")
+    with pytest.raises(pcdm.PCDMError) as e:
+        prob.run(x, 4, 1)
+    assert e.value.status == pcdm.PCDM_EINVAL
+    x = torch.zeros(40, device=dev)
+    with pytest.raises(pcdm.PCDMError) as e:
+        prob.run(x, 40, 200, beta_override=1e-30, variant="grid")
+    assert e.value.status == pcdm.PCDM_EDIVERGED
+    prob.close()
