@@ -61,7 +61,10 @@ typedef enum {
     PCDM_VARIANT_AUTO = 0, /* pick by problem size                                      */
     PCDM_VARIANT_GRID = 1, /* persistent cooperative grid, r in HBM/L2, grid barriers    */
     PCDM_VARIANT_SMEM = 2, /* one CTA, A, r, x, L resident in shared memory (small A)    */
-    PCDM_VARIANT_BLOCK = 3 /* one CTA, data in HBM/L2, __syncthreads barriers            */
+    PCDM_VARIANT_BLOCK = 3, /* one CTA, data in HBM/L2, __syncthreads barriers           */
+    PCDM_VARIANT_PACKED = 4 /* persistent grid on packed column blocks (one coalesced line
+                               per column); one barrier per iteration with double-buffered
+                               r when 2r fits in L2, else two.  Needs max column length <= 62 */
 } pcdm_variant;
 
 typedef struct {

@@ -77,6 +77,33 @@ struct IterLaunch {
     size_t smem;
 };
 
+// ---- packed-block hot loop (kernels_packed.cu)
+struct PackedParams {
+    const int4* blocks;   // [n][G] 16-byte chunks: {L, len, 0, 0}, then (row, val) pairs
+    float* x;
+    float* r0;            // residual buffer (TWO_BARRIER: the residual)
+    float* r1;            // second buffer (ONE_BARRIER only)
+    const int* slots;     // [iters][tau]
+    int64_t tau;
+    int64_t iters;
+    int64_t k0;           // run-local index of the first iteration of this launch
+    float beta;
+    float lambda;
+    int* nz_idx;          // [3][tau]
+    float* nz_delta;      // [3][tau]
+    int* nz_count;        // [3]
+    unsigned* barrier;
+    int* flags;
+    unsigned long long* nz_total;
+};
+int packed_lanes(int64_t max_len);
+cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
+                        int4* blocks, cudaStream_t st, int sms, int64_t* launches);
+int packed_ctas(int G, bool one_barrier, int sms);
+cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
+                          int64_t* launches);
+
 // Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
 IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device);
 cudaError_t launch_iter(const IterLaunch& L, const IterParams& P, cudaStream_t st, int64_t* launches);

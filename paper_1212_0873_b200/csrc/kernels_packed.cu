@@ -1,0 +1,255 @@
+// kernels_packed.cu -- the PCDM1 hot loop on packed column blocks (PACKED variant).
+//
+// Why: on B200 a random global access costs one DRAM line activation whatever
+// its width (measured: ~54 G random accesses/s from a 400 MB array, the same
+// with 64 B or 128 B L2 fetches), so the hot loop is bounded by the number of
+// distinct random lines touched per sampled column, not by bytes.  The CSC
+// layout touches colptr, rowidx, val, L and x on separate lines (4-6 random
+// lines) besides the c gathers of r.  Here column i is one slot of G x 16 B:
+//
+//   chunk 0       { L_i (f32), len (i32), 0, 0 }
+//   chunk t >= 1  { row_{2t-2}, val_{2t-2}, row_{2t-1}, val_{2t-1} }   (pairs beyond len unused)
+//
+// with G = pow2 >= 1 + ceil(maxlen/2) lanes per column: one coalesced
+// G x 16 B load per column (128 B for c = 10), each lane then gathers <= 2
+// entries of r.  The arithmetic is the same synchronous PCDM1 step as
+// kernels_iter.cu (alg:PCD1 PAPER.md:177-186; g_i = a_i^T r_k, soft-threshold
+// block update eq:h(x) PAPER.md:214-216).
+//
+// Barrier schemes:
+//   TWO_BARRIER  one residual buffer: phase A (gathers, steps, list of nonzero
+//                steps) | barrier | phase B (r += delta a_i for the list) | barrier.
+//   ONE_BARRIER  two residual buffers P = r_k (read-only in iteration k) and
+//                Q = r_{k-1}: iteration k gathers from P and scatters both its
+//                own steps Delta_k and the previous iteration's list Delta_{k-1}
+//                into Q, so after ONE barrier Q = r_{k-1} + Delta_{k-1} + Delta_k
+//                = r_{k+1} and the buffers swap.  Used when 2 r fits in L2.
+// Step lists rotate over 3 buffers (append k%3, replay (k-1)%3, reset (k+1)%3).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace pcdm;
+using namespace pcdm_internal;
+
+namespace {
+
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <int G>
+__device__ __forceinline__ unsigned gmask_of() {
+    if constexpr (G == 32) {
+        return 0xffffffffu;
+    } else {
+        const unsigned lane = threadIdx.x & 31;
+        return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+    }
+}
+
+// r[row] += val * d for this lane's (<= 2) pairs of the chunk.
+__device__ __forceinline__ void scatter_chunk(float* r, const int4 c, int pair0, int len, float d) {
+    if (pair0 < len) red_add_f32(r + c.x, __int_as_float(c.y) * d);
+    if (pair0 + 1 < len) red_add_f32(r + c.z, __int_as_float(c.w) * d);
+}
+
+template <int G, bool ONE_BARRIER>
+__global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P) {
+    const int t = threadIdx.x & (G - 1);  // lane within the column group
+    const unsigned gm = gmask_of<G>();
+    const int src = (threadIdx.x & 31) & ~(G - 1);
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int pair0 = 2 * (t - 1);
+    unsigned bar_target = 0;
+    const int64_t tau = P.tau;
+
+    for (int64_t it = 0; it < P.iters; ++it) {
+        const int64_t k = P.k0 + it;
+        const int cur = (int)(k % 3), prev = (int)((k + 2) % 3), next = (int)((k + 1) % 3);
+        const float* rP = (ONE_BARRIER && (k & 1)) ? P.r1 : P.r0;
+        float* rQ = (ONE_BARRIER && (k & 1)) ? P.r0 : P.r1;
+        const int* S = P.slots + it * tau;
+        if (blockIdx.x == 0 && threadIdx.x == 0) P.nz_count[next] = 0;
+
+        // ---------------- phase A: one coalesced block load + <= 2 gathers per lane
+        for (int64_t j = gid; j < tau; j += ngroups) {
+            const int i = ld_stream_s32(S + j);
+            float xi = 0.0f;
+            if (t == 0) xi = ld_l2_f32(P.x + i);
+            const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+            const int len = __shfl_sync(gm, c.y, src);
+            float acc = 0.0f;
+            if (t > 0) {
+                const float ra = pair0 < len ? ld_l2_f32(rP + c.x) : 0.0f;
+                const float rb = pair0 + 1 < len ? ld_l2_f32(rP + c.z) : 0.0f;
+                acc = fmaf(__int_as_float(c.y), ra, __int_as_float(c.w) * rb);
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gm, acc, o);
+            float d = 0.0f;
+            if (t == 0) {
+                const float xp = prox_l1(xi, acc, P.beta * __int_as_float(c.x), P.lambda);
+                d = xp - xi;
+                if (d != 0.0f) {
+                    if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
+                    P.x[i] = xp;
+                    const int pos = atomicAdd(P.nz_count + cur, 1);
+                    P.nz_idx[cur * tau + pos] = i;
+                    P.nz_delta[cur * tau + pos] = d;
+                }
+            }
+            if (ONE_BARRIER) {
+                d = __shfl_sync(gm, d, src);
+                if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d);
+            }
+        }
+        if (ONE_BARRIER) {
+            // replay the previous iteration's nonzero steps into Q
+            const int cntp = ld_l2_s32(P.nz_count + prev);
+            for (int64_t e = gid; e < cntp; e += ngroups) {
+                const int i = ld_l2_s32(P.nz_idx + prev * tau + e);
+                const float d = ld_l2_f32(P.nz_delta + prev * tau + e);
+                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int len = __shfl_sync(gm, c.y, src);
+                if (t > 0) scatter_chunk(rQ, c, pair0, len, d);
+            }
+            grid_barrier(P.barrier, bar_target);
+        } else {
+            grid_barrier(P.barrier, bar_target);
+            const int cnt = ld_l2_s32(P.nz_count + cur);
+            for (int64_t e = gid; e < cnt; e += ngroups) {
+                const int i = ld_l2_s32(P.nz_idx + cur * tau + e);
+                const float d = ld_l2_f32(P.nz_delta + cur * tau + e);
+                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int len = __shfl_sync(gm, c.y, src);
+                if (t > 0) scatter_chunk(P.r0, c, pair0, len, d);
+            }
+            grid_barrier(P.barrier, bar_target);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            const int cnt = ld_l2_s32(P.nz_count + cur);
+            if (cnt) atomicAdd(P.nz_total, (unsigned long long)cnt);
+        }
+    }
+}
+
+// Pack the CSC into blocks: one thread per (column, chunk).
+__global__ void pack_kernel(int64_t n, int G, const long long* __restrict__ colptr, const int* __restrict__ rowidx,
+                            const float* __restrict__ val, const float* __restrict__ L, int4* __restrict__ blocks) {
+    const int64_t total = n * G;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / G;
+        const int t = (int)(q - i * G);
+        const long long s = colptr[i];
+        const int len = (int)(colptr[i + 1] - s);
+        int4 c;
+        if (t == 0) {
+            c = make_int4(__float_as_int(L[i]), len, 0, 0);
+        } else {
+            const int p0 = 2 * (t - 1);
+            c.x = p0 < len ? rowidx[s + p0] : 0;
+            c.y = p0 < len ? __float_as_int(val[s + p0]) : 0;
+            c.z = p0 + 1 < len ? rowidx[s + p0 + 1] : 0;
+            c.w = p0 + 1 < len ? __float_as_int(val[s + p0 + 1]) : 0;
+        }
+        blocks[q] = c;
+    }
+}
+
+__global__ void max_len_kernel(int64_t n, const long long* __restrict__ colptr, int* __restrict__ out) {
+    long long best = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        best = max(best, colptr[i + 1] - colptr[i]);
+    int b = best > 0x7fffffff ? 0x7fffffff : (int)best;
+    b = __reduce_max_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, b);
+}
+
+template <int G, bool ONE>
+cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
+    void* args[] = {(void*)&P};
+    return cudaLaunchCooperativeKernel((const void*)pcdm_packed_kernel<G, ONE>, dim3(ctas), dim3(kThreads), args, 0,
+                                       st);
+}
+
+template <bool ONE>
+const void* kernel_ptr(int G) {
+    switch (G) {
+        case 2: return (const void*)pcdm_packed_kernel<2, ONE>;
+        case 4: return (const void*)pcdm_packed_kernel<4, ONE>;
+        case 8: return (const void*)pcdm_packed_kernel<8, ONE>;
+        case 16: return (const void*)pcdm_packed_kernel<16, ONE>;
+        default: return (const void*)pcdm_packed_kernel<32, ONE>;
+    }
+}
+
+}  // namespace
+
+namespace pcdm_internal {
+
+int packed_lanes(int64_t max_len) {
+    const int64_t chunks = 1 + (max_len + 1) / 2;
+    int g = 2;
+    while (g < chunks) g <<= 1;
+    return g;
+}
+
+cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    int64_t b = (n + 255) / 256;
+    if (b > sms * 8) b = sms * 8;
+    max_len_kernel<<<(int)b, 256, 0, st>>>(n, (const long long*)colptr, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
+                        int4* blocks, cudaStream_t st, int sms, int64_t* launches) {
+    int64_t b = (n * G + 255) / 256;
+    if (b > sms * 16) b = sms * 16;
+    pack_kernel<<<(int)b, 256, 0, st>>>(n, G, (const long long*)colptr, rowidx, val, L, blocks);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+int packed_ctas(int G, bool one_barrier, int sms) {
+    int per_sm = 1;
+    const void* fn = one_barrier ? kernel_ptr<true>(G) : kernel_ptr<false>(G);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm * sms;
+}
+
+cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
+                          int64_t* launches) {
+    ++*launches;
+    if (one_barrier) {
+        switch (G) {
+            case 2: return launch_g<2, true>(ctas, P, st);
+            case 4: return launch_g<4, true>(ctas, P, st);
+            case 8: return launch_g<8, true>(ctas, P, st);
+            case 16: return launch_g<16, true>(ctas, P, st);
+            default: return launch_g<32, true>(ctas, P, st);
+        }
+    }
+    switch (G) {
+        case 2: return launch_g<2, false>(ctas, P, st);
+        case 4: return launch_g<4, false>(ctas, P, st);
+        case 8: return launch_g<8, false>(ctas, P, st);
+        case 16: return launch_g<16, false>(ctas, P, st);
+        default: return launch_g<32, false>(ctas, P, st);
+    }
+}
+
+}  // namespace pcdm_internal

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -56,7 +57,7 @@ bool is_device_ptr(const void* p) {
 struct Scalars {
     int flags;
     unsigned barrier;
-    int nz_count[2];
+    int nz_count[3];
     int max_out;
     int rounds_max;
     unsigned long long nz_total;
@@ -77,7 +78,12 @@ struct pcdm_problem {
     float* val = nullptr;
     float* b = nullptr;
     float* L = nullptr;
-    float* r = nullptr;
+    float* r = nullptr;        // residual (buffer 0)
+    float* r2 = nullptr;       // second residual buffer (one-barrier packed loop)
+    float* r_cur = nullptr;    // buffer holding the residual after the last run
+    int4* blocks = nullptr;    // packed column blocks (PACKED variant), [n][packed_G]
+    int packed_G = 0;          // 0: no packed copy (a column longer than 62 entries)
+    int64_t max_len = 0;
     double* r64 = nullptr;
     float* xbuf = nullptr;     // device iterate when the caller passes host x
     Scalars* sc = nullptr;     // device scalars
@@ -110,6 +116,8 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->L);
     cudaFree(p->r);
     cudaFree(p->r64);
+    cudaFree(p->r2);
+    cudaFree(p->blocks);
     cudaFree(p->xbuf);
     cudaFree(p->sc);
     cudaFree(p->nz_idx);
@@ -229,8 +237,10 @@ pcdm_status sampler_workspace(void** mem, size_t* cap, int64_t n, int64_t tau, i
 }
 
 int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
+    // keep one chunk's sampler tables + slots within ~40 MB so the sampler's random
+    // atomics stay in L2 (126 MB) instead of going to HBM
     const size_t per = sampler_bytes_per_iter(n, tau, nullptr) + (size_t)tau * 4;
-    const size_t budget = (size_t)512 << 20;
+    const size_t budget = (size_t)40 << 20;
     int64_t c = (int64_t)std::max<size_t>(1, budget / per);
     c = std::min<int64_t>(c, 8192);
     return std::min<int64_t>(c, std::max<int64_t>(iters, 1));
@@ -284,9 +294,25 @@ pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         cudaFree(counts);
         if (s != PCDM_OK) break;
         p->omega = hs.max_out;
+        // packed column blocks for the PACKED hot loop (skipped if a column is too long
+        // or the device cannot hold the copy)
+        if ((e = launch_max_len(n, p->colptr, &p->sc->max_out, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "max len"); break; }
+        if ((s = read_scalars(p, &hs, st)) != PCDM_OK) break;
+        p->max_len = hs.max_out;
+        if (p->max_len <= 62 && !getenv("PCDM_NO_PACK")) {
+            const int G = packed_lanes(p->max_len);
+            if (cudaMalloc((void**)&p->blocks, (size_t)n * G * 16) == cudaSuccess) {
+                p->packed_G = G;
+                if ((e = launch_pack(n, G, p->colptr, p->rowidx, p->val, p->L, p->blocks, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "pack"); break; }
+            } else {
+                cudaGetLastError();
+                p->blocks = nullptr;
+            }
+        }
         if ((e = cudaMalloc((void**)&p->r, sizeof(float) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc r"); break; }
         if ((e = cudaMalloc((void**)&p->r64, sizeof(double) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc r64"); break; }
         if ((e = cudaMemsetAsync(p->r, 0, sizeof(float) * m, st)) != cudaSuccess) { s = cuda_fail(e, "memset r"); break; }
+        p->r_cur = p->r;
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { s = cuda_fail(e, "create sync"); break; }
     } while (0);
     if (s != PCDM_OK) {
@@ -329,7 +355,9 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
     if (tau < 1 || tau > p->n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
     if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
     if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
-    if (variant < 0 || variant > 3) return fail(PCDM_EINVAL, "unknown variant %d", variant);
+    if (variant < 0 || variant > 4) return fail(PCDM_EINVAL, "unknown variant %d", variant);
+    if (variant == PCDM_VARIANT_PACKED && !p->packed_G)
+        return fail(PCDM_EINVAL, "PACKED variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
@@ -359,17 +387,35 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
     pcdm_beta(p, tau, &beta_d);
     if (beta_override > 0.0) beta_d = beta_override;
     const int64_t R = refresh_period(p->n, tau, refresh_every);
-    const IterLaunch plan = plan_iter(variant, p->m, p->n, p->nnz, tau, p->sms, p->device);
+    IterLaunch plan = plan_iter(variant == PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
+                                p->sms, p->device);
+    // AUTO: packed blocks whenever the shared-memory variant does not apply
+    const bool packed = p->packed_G > 0 &&
+                        (variant == PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
+    bool one_barrier = false;
+    if (packed) {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
+        one_barrier = 2 * 4 * p->m <= l2 / 4;
+        const char* ob = getenv("PCDM_ONE_BARRIER");
+        if (ob) one_barrier = atoi(ob) != 0;
+        if (one_barrier && !p->r2) CK(cudaMalloc((void**)&p->r2, sizeof(float) * p->m), "alloc r2");
+        plan.variant = PCDM_VARIANT_PACKED;
+        plan.lanes = p->packed_G;
+        plan.threads = 512;
+        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms);
+    }
     if (p->nz_cap < tau) {
         cudaFree(p->nz_idx);
         cudaFree(p->nz_delta);
         p->nz_idx = nullptr;
         p->nz_delta = nullptr;
         p->nz_cap = 0;
-        CK(cudaMalloc((void**)&p->nz_idx, sizeof(int) * 2 * tau), "alloc step list");
-        CK(cudaMalloc((void**)&p->nz_delta, sizeof(float) * 2 * tau), "alloc step list");
+        CK(cudaMalloc((void**)&p->nz_idx, sizeof(int) * 3 * tau), "alloc step list");
+        CK(cudaMalloc((void**)&p->nz_delta, sizeof(float) * 3 * tau), "alloc step list");
         p->nz_cap = tau;
     }
+    if (one_barrier) CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
     int64_t chunk = choose_chunk(p->n, tau, iters);
     if (R > 0) chunk = std::min(chunk, R);
     SamplerPlan sp;
@@ -394,6 +440,20 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
     P.nz_total = &p->sc->nz_total;
     P.m = p->m;
     P.n = p->n;
+    PackedParams Q{};
+    Q.blocks = p->blocks;
+    Q.x = xd;
+    Q.r0 = p->r;
+    Q.r1 = one_barrier ? p->r2 : nullptr;
+    Q.tau = tau;
+    Q.beta = (float)beta_d;
+    Q.lambda = (float)p->lambda;
+    Q.nz_idx = p->nz_idx;
+    Q.nz_delta = p->nz_delta;
+    Q.nz_count = p->sc->nz_count;
+    Q.barrier = &p->sc->barrier;
+    Q.flags = &p->sc->flags;
+    Q.nz_total = &p->sc->nz_total;
 
     int64_t done = 0;
     while (done < iters) {
@@ -403,14 +463,23 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
         CK(tm.begin(&ts), "event");
         CK(sample_chunk(sp.w, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
            "sampler");
-        // zero barrier counter and both step-list counters (contiguous in Scalars)
-        CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + 2 * sizeof(int), st), "memset barrier");
+        // zero the barrier counter; the generic kernel also restarts its step lists per
+        // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
+        CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed ? 0 : 3 * sizeof(int)), st),
+           "memset barrier");
         CK(tm.end(T_SAMPLER, ts), "event");
-        P.slots = sp.slots;
-        P.iters = c;
         int ti;
         CK(tm.begin(&ti), "event");
-        CK(launch_iter(plan, P, st, &launches), "iteration kernel");
+        if (packed) {
+            Q.slots = sp.slots;
+            Q.iters = c;
+            Q.k0 = done;
+            CK(launch_packed(p->packed_G, one_barrier, plan.ctas, Q, st, &launches), "packed iteration kernel");
+        } else {
+            P.slots = sp.slots;
+            P.iters = c;
+            CK(launch_iter(plan, P, st, &launches), "iteration kernel");
+        }
         CK(tm.end(T_ITER, ti), "event");
         ++stats.iter_launches;
         done += c;
@@ -418,10 +487,15 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
             int tr;
             CK(tm.begin(&tr), "event");
             if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) return s;
+            if (one_barrier) {
+                CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
+                CK(cudaMemsetAsync(p->sc->nz_count, 0, 3 * sizeof(int), st), "memset lists");
+            }
             CK(tm.end(T_SETUP, tr), "event");
             ++stats.refreshes;
         }
     }
+    p->r_cur = (one_barrier && (iters & 1)) ? p->r2 : p->r;
     int tx;
     CK(tm.begin(&tx), "event");
     if (!x_dev) CK(cudaMemcpyAsync(x, p->xbuf, sizeof(float) * p->n, cudaMemcpyDeviceToHost, st), "copy x out");
@@ -550,7 +624,7 @@ pcdm_status pcdm_row_counts(const pcdm_problem* p, int32_t* counts, void* stream
 pcdm_status pcdm_residual(const pcdm_problem* p, float* r, void* stream) {
     if (!p || !r) return fail(PCDM_EINVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    CK(cudaMemcpyAsync(r, p->r, sizeof(float) * p->m, cudaMemcpyDefault, st), "copy r");
+    CK(cudaMemcpyAsync(r, p->r_cur, sizeof(float) * p->m, cudaMemcpyDefault, st), "copy r");
     CK(cudaStreamSynchronize(st), "sync");
     return PCDM_OK;
 }

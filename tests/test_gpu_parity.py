@@ -101,7 +101,7 @@ def test_medium_config_full_run(gpu):
     inst = I.generate("medium", seed=0)
     out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 1024, 10_000, seed=0)
     assert_parity(out)
-    assert out["stats"]["variant"] == pcdm.VARIANTS["grid"]
+    assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
 
 
 @pytest.mark.parametrize("tau", [1 << 8, 1 << 12, 1 << 16])
@@ -232,4 +232,37 @@ def test_errors(gpu):
     with pytest.raises(pcdm.PCDMError) as e:
         prob.run(x, 40, 200, beta_override=1e-30, variant="grid")
     assert e.value.status == pcdm.PCDM_EDIVERGED
+    prob.close()
+
+
+# ------------------------------------------------------------------ packed-block loop
+@pytest.mark.parametrize("one_barrier", ["0", "1"])
+@pytest.mark.parametrize("lens_kind", ["uniform10", "uniform20", "ragged"])
+def test_packed_variant_both_barrier_schemes(gpu, monkeypatch, one_barrier, lens_kind):
+    monkeypatch.setenv("PCDM_ONE_BARRIER", one_barrier)
+    m, n = 5000, 4000
+    rng = np.random.default_rng(3)
+    lens = {"uniform10": np.full(n, 10), "uniform20": np.full(n, 20),
+            "ragged": rng.integers(0, 62, size=n)}[lens_kind]
+    if lens_kind == "ragged":
+        lens[:5] = 0
+        lens[5] = 62
+    c, r, v, b, lam = _ragged(m, n, lens, 8, lam_frac=0.05)
+    x0 = np.random.default_rng(4).normal(size=n) * (np.arange(n) % 7 == 0)
+    for tau, iters, refresh in ((1, 300, 0), (64, 200, 0), (1000, 40, 7), (4000, 5, -1)):
+        out = run_both(c, r, v, b, lam, m, tau, iters, seed=tau, variant="packed", x0=x0,
+                       refresh_every=refresh)
+        assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
+        assert_parity(out)
+        np.testing.assert_allclose(out["r_gpu"], out["res"].r, rtol=0,
+                                   atol=1e-4 * np.max(np.abs(out["res"].r)))
+
+
+def test_packed_rejected_for_long_columns(gpu):
+    c, r, v, b, lam = _ragged(300, 20, [100] + [3] * 19, 2)
+    prob = pcdm.Problem(300, 20, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), lam)
+    with pytest.raises(pcdm.PCDMError) as e:
+        prob.run(torch.zeros(20, device=gpu), 4, 1, variant="packed")
+    assert e.value.status == pcdm.PCDM_EINVAL
+    prob.run(torch.zeros(20, device=gpu), 4, 1)  # AUTO falls back to a valid variant
     prob.close()
