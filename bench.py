@@ -39,6 +39,8 @@ from paper_1212_0873_b200 import instances as I  # noqa: E402
 
 METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline) at 1 B200"
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
+VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed"}
+KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel"}
 # oracle iterations per reference step / cpu_baseline sample, per config
 REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4}
 CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24}
@@ -365,7 +367,7 @@ def bench_ours(args, world, rank, local):
         "effective_GBps": value * avg_c * BYTES_PER_NNZ / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "pcdm_iter_kernel", "algorithmic_bytes_per_launch": alg_bytes_launch,
+                     "kernel": KERNEL_OF_VARIANT.get(st0["variant"], "?"), "algorithmic_bytes_per_launch": alg_bytes_launch,
                      "launch_ms": launch_ms, "iters_per_launch": iters_per_launch,
                      "share_of_step": it_ms / max(sum(step_ms), 1e-9)},
         "breakdown_ms_per_step": {"iteration_kernel": it_ms / K, "sampler": samp_ms / K, "setup": setup_ms / K},
@@ -375,7 +377,7 @@ def bench_ours(args, world, rank, local):
         "cpu_baseline": cpu,
         "omega": prob.omega, "beta": prob.beta(tau), "F_final": F_final,
         "nonzero_step_frac": nz / (K * tau * iters),
-        "variant": {1: "grid", 2: "smem", 3: "block"}.get(st0["variant"], "?"),
+        "variant": VARIANT_NAMES.get(st0["variant"], "?"),
         "grid": {"ctas": st0["grid_ctas"], "threads": st0["threads_per_cta"], "lanes_per_column": st0["lanes_per_column"]},
         "setup_s": {"generate": gen_s, "create": create_s},
         "context": "paper: 2e10-nnz LASSO in ~2 h on 24 cores (~4.8e6 updates/s, asynchronous, PAPER.md:1237,1248)",
