@@ -243,6 +243,7 @@ int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
     const size_t budget = (size_t)40 << 20;
     int64_t c = (int64_t)std::max<size_t>(1, budget / per);
     c = std::min<int64_t>(c, 8192);
+    if (const char* fc = getenv("PCDM_CHUNK")) c = std::max<int64_t>(1, atoll(fc));  // tests / tuning
     return std::min<int64_t>(c, std::max<int64_t>(iters, 1));
 }
 

@@ -266,3 +266,15 @@ def test_packed_rejected_for_long_columns(gpu):
     assert e.value.status == pcdm.PCDM_EINVAL
     prob.run(torch.zeros(20, device=gpu), 4, 1)  # AUTO falls back to a valid variant
     prob.close()
+
+
+# ------------------------------------------------------------------ many launches per run
+@pytest.mark.parametrize("variant", ["packed", "grid"])
+def test_many_chunks_per_run(gpu, monkeypatch, variant):
+    # small chunks force many sampler passes and iteration-kernel launches per run
+    monkeypatch.setenv("PCDM_CHUNK", "3")
+    c, r, v, b, lam = _ragged(3000, 2500, np.full(2500, 12), 12)
+    for tau, iters, refresh in ((256, 61, 0), (2500, 7, 4), (33, 200, -1)):
+        out = run_both(c, r, v, b, lam, 3000, tau, iters, seed=5, variant=variant, refresh_every=refresh)
+        assert_parity(out)
+        assert out["stats"]["iter_launches"] >= iters // 3
