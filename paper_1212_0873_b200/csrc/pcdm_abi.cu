@@ -240,7 +240,8 @@ int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
     // keep one chunk's sampler tables + slots within ~40 MB so the sampler's random
     // atomics stay in L2 (126 MB) instead of going to HBM
     const size_t per = sampler_bytes_per_iter(n, tau, nullptr) + (size_t)tau * 4;
-    const size_t budget = (size_t)40 << 20;
+    size_t budget = (size_t)64 << 20;
+    if (const char* mb = getenv("PCDM_SAMPLER_MB")) budget = (size_t)std::max(1, atoi(mb)) << 20;
     int64_t c = (int64_t)std::max<size_t>(1, budget / per);
     c = std::min<int64_t>(c, 8192);
     if (const char* fc = getenv("PCDM_CHUNK")) c = std::max<int64_t>(1, atoll(fc));  // tests / tuning
