@@ -59,6 +59,16 @@ def test_sampler_bitexact_config_shapes(gpu, cfg, tau, count):
         assert np.array_equal(got[k], oracle.sample(0, k, tau, n)), k
 
 
+@pytest.mark.parametrize("n,tau,count", [(9000, 4400, 4), (8193, 4096, 3), (1 << 20, 1 << 17, 3), (50000, 4096, 20)])
+def test_sampler_bitexact_large_tau(gpu, n, tau, count):
+    # larger tau, and n close to 2 tau (many ownership rounds), over several iterations
+    for seed in (0, 5):
+        got = np.zeros(count * tau, dtype=np.int32)
+        pcdm.pcdm_sample(n, tau, seed, 77, count, got, stream=0)
+        for k in range(count):
+            assert np.array_equal(got[k * tau:(k + 1) * tau], oracle.sample(seed, 77 + k, tau, n)), (seed, k)
+
+
 def test_sampler_high_collision_rounds(gpu):
     # tau close to n/2 forces many ownership rounds; still bit-exact
     n, tau, count = 4001, 2000, 6
