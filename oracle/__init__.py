@@ -67,6 +67,15 @@ def _load():
     lib.or_run.argtypes = [i64, i64, P, P, P, P, f64, P, f64, P, i64, i64, u64, i64, i64,
                            P, P, ctypes.POINTER(ctypes.c_double)]
     lib.or_run.restype = i32
+    lib.or_sample_kind.argtypes = [i32, u64, i64, i64, i64, f64, P, P]
+    lib.or_sample_kind.restype = i32
+    lib.or_moments.argtypes = [i32, i64, i64, f64, P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    lib.or_moments.restype = i32
+    lib.or_beta_du.argtypes = [i64, i64, f64, f64]
+    lib.or_beta_du.restype = f64
+    lib.or_run_kind.argtypes = [i64, i64, P, P, P, P, f64, P, f64, P, i32, i64, f64, P, i64, u64, i64, i64,
+                                P, P, ctypes.POINTER(ctypes.c_double)]
+    lib.or_run_kind.restype = i32
     _lib = lib
     return lib
 
@@ -104,6 +113,51 @@ def sample(seed: int, k: int, tau: int, n: int) -> np.ndarray:
     if rc != 0:
         raise ValueError("or_sample failed (rc=%d)" % rc)
     return out
+
+
+# ---------------------------------------------------------------- other DU samplings (NEXT-1)
+KINDS = {"nice": 0, "independent": 1, "binomial": 2, "du": 3}
+
+
+class Sampling:
+    """A doubly uniform sampling: kind in KINDS, tau processors /
+    slots, p_b for binomial, q[0..tau] (size law) for du."""
+
+    def __init__(self, kind="nice", tau=1, p_b=1.0, q=None):
+        self.kind, self.tau, self.p_b = kind, int(tau), float(p_b)
+        self.q = None if q is None else np.ascontiguousarray(q, dtype=np.float64)
+        if kind == "du" and (self.q is None or self.q.size != self.tau + 1):
+            raise ValueError("du sampling needs q[0..tau]")
+
+    def _q(self):
+        return _ptr(self.q) if self.q is not None else None
+
+
+def sample_kind(s: Sampling, seed: int, k: int, n: int) -> np.ndarray:
+    """Slot array of S_k for sampling s (idle slots are -1)."""
+    out = np.empty(s.tau, dtype=np.int32)
+    rc = _load().or_sample_kind(KINDS[s.kind], seed, k, s.tau, n, s.p_b, s._q(), _ptr(out))
+    if rc != 0:
+        raise ValueError("or_sample_kind failed (rc=%d)" % rc)
+    return out
+
+
+def moments(s: Sampling, n: int):
+    """(E|S|, E|S|^2) of the sampling."""
+    e1, e2 = ctypes.c_double(), ctypes.c_double()
+    rc = _load().or_moments(KINDS[s.kind], s.tau, n, s.p_b, s._q(), ctypes.byref(e1), ctypes.byref(e2))
+    if rc != 0:
+        raise ValueError("or_moments failed")
+    return e1.value, e2.value
+
+
+def beta_du(omega_: int, n: int, e1: float, e2: float) -> float:
+    """thm:ESO-DU: beta = 1 + (omega-1)(E|S|^2/E|S| - 1)/max(1,n-1)."""
+    return float(_load().or_beta_du(omega_, n, e1, e2))
+
+
+def beta_sampling(omega_: int, n: int, s: Sampling) -> float:
+    return beta_du(omega_, n, *moments(s, n))
 
 
 def row_counts(m: int, rowidx) -> np.ndarray:
@@ -173,7 +227,7 @@ class RunResult:
 
 def run(m, colptr, rowidx, val, b, lam, tau, iters, seed, x0=None, first_iter=0,
         refresh_every=0, beta_override=None, omega_override=None, L=None,
-        keep_slots=False) -> RunResult:
+        keep_slots=False, sampling: Sampling = None) -> RunResult:
     """Synchronous PCDM1 (alg:PCD1) for LASSO, O1..O8 of SURVEY 8(c).
 
     omega_override / L let a caller hand in the oracle's own omega / L computed
@@ -185,14 +239,27 @@ def run(m, colptr, rowidx, val, b, lam, tau, iters, seed, x0=None, first_iter=0,
     lib = _load()
     om = omega(m, rowidx) if omega_override is None else int(omega_override)
     Lv = col_norms(colptr, val) if L is None else np.ascontiguousarray(L, dtype=np.float64)
-    bt = beta(om, tau, n) if beta_override is None else float(beta_override)
+    if sampling is not None:
+        tau = sampling.tau
+    if beta_override is not None:
+        bt = float(beta_override)
+    elif sampling is None or sampling.kind == "nice":
+        bt = beta(om, tau, n)
+    else:
+        bt = beta_sampling(om, n, sampling)
     x = np.zeros(n, dtype=np.float64) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
     r = np.empty(m, dtype=np.float64)
     slots = np.empty(iters * tau, dtype=np.int32) if keep_slots else None
     secs = ctypes.c_double(0.0)
-    rc = lib.or_run(m, n, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(b), lam, _ptr(Lv), bt,
-                    _ptr(x), tau, iters, seed, first_iter, refresh_every, _ptr(r),
-                    _ptr(slots) if keep_slots else None, ctypes.byref(secs))
+    if sampling is None or sampling.kind == "nice":
+        rc = lib.or_run(m, n, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(b), lam, _ptr(Lv), bt,
+                        _ptr(x), tau, iters, seed, first_iter, refresh_every, _ptr(r),
+                        _ptr(slots) if keep_slots else None, ctypes.byref(secs))
+    else:
+        rc = lib.or_run_kind(m, n, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(b), lam, _ptr(Lv), bt,
+                             _ptr(x), KINDS[sampling.kind], tau, sampling.p_b, sampling._q(), iters, seed,
+                             first_iter, refresh_every, _ptr(r), _ptr(slots) if keep_slots else None,
+                             ctypes.byref(secs))
     if rc < 0:
         raise ValueError("or_run failed (rc=%d)" % rc)
     if rc == 1:

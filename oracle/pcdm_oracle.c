@@ -143,6 +143,148 @@ int or_sample(uint64_t seed, int64_t k, int64_t tau, int64_t n, int32_t *slots,
     return rc;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Other doubly uniform samplings.      */
+/* Each returns tau slots; an idle slot (a processor that updates nothing) is  */
+/* -1.  Readings (R16-R18) fix the concrete random stream.           */
+/* ------------------------------------------------------------------------ */
+enum { OR_NICE = 0, OR_INDEPENDENT = 1, OR_BINOMIAL = 2, OR_DU = 3 };
+
+/* 64-bit word of counter (j, k, 0, tag) under key (lo32 seed, hi32 seed). */
+static uint64_t or_word(uint64_t seed, uint32_t k, uint32_t j, uint32_t tag)
+{
+    uint32_t ctr[4] = { j, k, 0u, tag };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t out[4];
+    or_philox4x32_10(ctr, key, out);
+    return ((uint64_t)out[1] << 32) | (uint64_t)out[0];
+}
+
+/* floor(p * 2^64) for 0 <= p < 1; UINT64_MAX + "always" for p >= 1 (flag). */
+static uint64_t or_threshold(double p, int *always)
+{
+    *always = 0;
+    if (p >= 1.0) { *always = 1; return UINT64_MAX; }
+    if (p <= 0.0) return 0;
+    return (uint64_t)(p * 18446744073709551616.0); /* 2^64: exact scaling, then truncation */
+}
+
+/* tau-independent sampling: processor j = 0..tau-1 picks
+ * the first accepted draw of counters (j, k, rho, tag 3), rho = 0,1,...,
+ * independently of the others; "if two or more processors pick the same block,
+ * all but one will be idle": the lowest j keeps it (reading R16). */
+int or_sample_independent(uint64_t seed, int64_t k, int64_t tau, int64_t n, int32_t *slots)
+{
+    if (n < 1 || tau < 1 || tau > n || k < 0 || k > 0xFFFFFFFFLL || n > 0x7FFFFFFFLL) return -1;
+    unsigned char *taken = (unsigned char *)calloc((size_t)n, 1);
+    if (!taken) return -1;
+    for (int64_t j = 0; j < tau; ++j) {
+        uint64_t v = 0;
+        uint32_t rho = 0;
+        while (!or_draw(seed, (uint32_t)k, rho, (uint32_t)j, 3u, (uint64_t)n, &v)) ++rho;
+        if (taken[v]) {
+            slots[j] = -1;
+        } else {
+            taken[v] = 1;
+            slots[j] = (int32_t)v;
+        }
+    }
+    free(taken);
+    return 0;
+}
+
+/* (tau, p_b)-binomial sampling, Case 2 of PAPER.md:452-455: a tau-nice set is
+ * assigned to tau processors, processor j is available with probability p_b
+ * independently (word of counter (j, k, 0, tag 4) < floor(p_b 2^64)); busy
+ * processors are idle (reading R17). */
+int or_sample_binomial(uint64_t seed, int64_t k, int64_t tau, int64_t n, double p_b, int32_t *slots)
+{
+    int rc = or_sample(seed, k, tau, n, slots, NULL);
+    if (rc != 0) return rc;
+    int always;
+    uint64_t T = or_threshold(p_b, &always);
+    for (int64_t j = 0; j < tau; ++j)
+        if (!always && !(or_word(seed, (uint32_t)k, (uint32_t)j, 4u) < T)) slots[j] = -1;
+    return 0;
+}
+
+/* Doubly uniform sampling with size law q[0..tau] (eq:p(S)):
+ * |S| = K is the smallest K with u < floor(min(1, q_0 + ... + q_K) 2^64), u the
+ * word of counter (0, k, 0, tag 5) (cumulative sums in fp64, left to right;
+ * the last one counts as 1); S = the first K slots of the tau-nice slot array
+ * (uniform over ordered tau-tuples, so its K-prefix is uniform over K-subsets;
+ * needs 2 tau <= n: the complement path's sorted output has no such property)
+ * (reading R18). */
+int or_sample_du(uint64_t seed, int64_t k, int64_t tau, int64_t n, const double *q, int32_t *slots)
+{
+    if (2 * tau > n) return -1;
+    int rc = or_sample(seed, k, tau, n, slots, NULL);
+    if (rc != 0) return rc;
+    uint64_t u = or_word(seed, (uint32_t)k, 0u, 5u);
+    double cum = 0.0;
+    int64_t K = tau;
+    for (int64_t s = 0; s < tau; ++s) {
+        cum += q[s];
+        int always;
+        uint64_t T = or_threshold(cum, &always);
+        if (always || u < T) { K = s; break; }
+    }
+    for (int64_t j = K; j < tau; ++j) slots[j] = -1;
+    return 0;
+}
+
+int or_sample_kind(int kind, uint64_t seed, int64_t k, int64_t tau, int64_t n, double p_b, const double *q,
+                   int32_t *slots)
+{
+    switch (kind) {
+    case OR_NICE: return or_sample(seed, k, tau, n, slots, NULL);
+    case OR_INDEPENDENT: return or_sample_independent(seed, k, tau, n, slots);
+    case OR_BINOMIAL: return or_sample_binomial(seed, k, tau, n, p_b, slots);
+    case OR_DU: return or_sample_du(seed, k, tau, n, q, slots);
+    default: return -1;
+    }
+}
+
+/* First two moments of |S| (E|S|, E|S|^2) for each sampling:
+ *   nice: tau, tau^2;
+ *   independent: occupancy of n bins by tau balls, E|S| = n(1 - (1-1/n)^tau),
+ *     E|S|^2 = E|S| + n(n-1)(1 - 2(1-1/n)^tau + (1-2/n)^tau)   (the law is the
+ *     q_k of PAPER.md:440-444; tests pin these against that recursion);
+ *   binomial: tau p_b and tau p_b (1 + tau p_b - p_b);
+ *   DU: sum_k k q_k and sum_k k^2 q_k. */
+int or_moments(int kind, int64_t tau, int64_t n, double p_b, const double *q, double *e1, double *e2)
+{
+    double t = (double)tau, nn = (double)n;
+    switch (kind) {
+    case OR_NICE: *e1 = t; *e2 = t * t; return 0;
+    case OR_INDEPENDENT: {
+        double a = pow(1.0 - 1.0 / nn, t);
+        double b = (n >= 2) ? pow(1.0 - 2.0 / nn, t) : 0.0;
+        *e1 = nn * (1.0 - a);
+        *e2 = *e1 + nn * (nn - 1.0) * (1.0 - 2.0 * a + b);
+        return 0;
+    }
+    case OR_BINOMIAL: *e1 = t * p_b; *e2 = t * p_b * (1.0 + t * p_b - p_b); return 0;
+    case OR_DU: {
+        double s1 = 0.0, s2 = 0.0;
+        for (int64_t kk = 0; kk <= tau; ++kk) { s1 += (double)kk * q[kk]; s2 += (double)kk * (double)kk * q[kk]; }
+        *e1 = s1; *e2 = s2;
+        return 0;
+    }
+    default: return -1;
+    }
+}
+
+/* ESO constant for a doubly uniform sampling (thm:ESO-DU, PAPER.md:955-960;
+ * tbl:ESO PAPER.md:339,346):
+ *   beta = 1 + (omega-1)(E|S|^2 / E|S| - 1) / max(1, n-1). */
+double or_beta_du(int64_t omega, int64_t n, double e1, double e2)
+{
+    double denom = (double)(n - 1 > 1 ? n - 1 : 1);
+    if (e1 <= 0.0) return 1.0;
+    return 1.0 + (double)(omega - 1) * (e2 / e1 - 1.0) / denom;
+}
+
 /* O1: degree of partial separability for f = 1/2||Ax-b||^2 with unit blocks:
  * omega = max_j ||A_j||_0, the maximum number of (stored) entries in a row
  * (eq:omega PAPER.md:54; LASSO PAPER.md:303; reading R#3: count
@@ -254,10 +396,11 @@ static double now_seconds(void)
  * x: double[n] in/out.  r_out (double[m]) / slots_out (int32[iters*tau]) /
  * loop_seconds may be NULL.  Returns 0, or <0 on bad args/sampler failure,
  * or 1 if a non-finite delta occurred (divergence). */
-int or_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
-           const float *val, const float *b, double lambda, const double *L, double beta,
-           double *x, int64_t tau, int64_t iters, uint64_t seed, int64_t first_iter,
-           int64_t refresh_every, double *r_out, int32_t *slots_out, double *loop_seconds)
+int or_run_kind(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
+                const float *val, const float *b, double lambda, const double *L, double beta,
+                double *x, int kind, int64_t tau, double p_b, const double *q, int64_t iters,
+                uint64_t seed, int64_t first_iter, int64_t refresh_every, double *r_out,
+                int32_t *slots_out, double *loop_seconds)
 {
     if (m < 1 || n < 1 || tau < 1 || tau > n || iters < 0 || first_iter < 0) return -1;
     double *r = (double *)malloc(sizeof(double) * (size_t)m);
@@ -273,12 +416,14 @@ int or_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
     double t0 = now_seconds();
     for (int64_t it = 0; it < iters && rc == 0; ++it) {
         int64_t k = first_iter + it;
-        int src = or_sample(seed, k, tau, n, S, taken); /* O5 */
+        int src = (kind == OR_NICE) ? or_sample(seed, k, tau, n, S, taken) /* O5 */
+                                    : or_sample_kind(kind, seed, k, tau, n, p_b, q, S);
         if (src != 0) { rc = -2; break; }
         if (slots_out) memcpy(slots_out + it * tau, S, sizeof(int32_t) * (size_t)tau);
 
         for (int64_t j = 0; j < tau; ++j) { /* O6: read phase */
             int64_t i = S[j];
+            if (i < 0) continue; /* idle processor */
             double g = 0.0;
             for (int64_t p = colptr[i]; p < colptr[i + 1]; ++p)
                 g += (double)val[p] * r[rowidx[p]];
@@ -287,6 +432,7 @@ int or_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
         }
         for (int64_t j = 0; j < tau; ++j) { /* O7: write phase */
             int64_t i = S[j];
+            if (i < 0) continue;
             double delta = xplus[j] - x[i];
             x[i] = xplus[j];
             for (int64_t p = colptr[i]; p < colptr[i + 1]; ++p)
@@ -300,4 +446,14 @@ int or_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
     if (r_out) memcpy(r_out, r, sizeof(double) * (size_t)m);
     free(r); free(S); free(xplus); free(taken);
     return rc;
+}
+
+/* Synchronous PCDM1 with the tau-nice sampling (the north_star path). */
+int or_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
+           const float *val, const float *b, double lambda, const double *L, double beta,
+           double *x, int64_t tau, int64_t iters, uint64_t seed, int64_t first_iter,
+           int64_t refresh_every, double *r_out, int32_t *slots_out, double *loop_seconds)
+{
+    return or_run_kind(m, n, colptr, rowidx, val, b, lambda, L, beta, x, OR_NICE, tau, 0.0, NULL, iters,
+                       seed, first_iter, refresh_every, r_out, slots_out, loop_seconds);
 }

@@ -60,3 +60,55 @@ def sample(seed, k, tau, n):
     if comp:
         return [v for v in range(n) if v not in owner]
     return slot_val
+
+
+# ---------------------------------------------------------------- other DU samplings (NEXT-1)
+def word(seed, k, j, tag):
+    out = philox4x32_10([j, k, 0, tag], [seed & M32, (seed >> 32) & M32])
+    return (out[1] << 32) | out[0]
+
+
+def threshold(p):
+    """(always, floor(p * 2^64)) with exact rational arithmetic on the double p."""
+    from fractions import Fraction
+    if p >= 1.0:
+        return True, 0
+    if p <= 0.0:
+        return False, 0
+    return False, int(Fraction(p) * (1 << 64))
+
+
+def sample_independent(seed, k, tau, n):
+    picked = set()
+    out = []
+    for j in range(tau):
+        rho = 0
+        while True:
+            v = draw(seed, k, rho, j, 3, n)
+            if v is not None:
+                break
+            rho += 1
+        out.append(-1 if v in picked else v)
+        picked.add(v)
+    return out
+
+
+def sample_binomial(seed, k, tau, n, p_b):
+    s = sample(seed, k, tau, n)
+    always, T = threshold(p_b)
+    return [v if always or word(seed, k, j, 4) < T else -1 for j, v in enumerate(s)]
+
+
+def sample_du(seed, k, tau, n, q):
+    assert 2 * tau <= n
+    s = sample(seed, k, tau, n)
+    u = word(seed, k, 0, 5)
+    cum = 0.0
+    K = tau
+    for size in range(tau):
+        cum += float(q[size])        # same left-to-right fp64 cumulative sums
+        always, T = threshold(cum)
+        if always or u < T:
+            K = size
+            break
+    return [v if j < K else -1 for j, v in enumerate(s)]
