@@ -67,6 +67,38 @@ typedef enum {
                                r when 2r fits in L2, else two.  Needs max column length <= 62 */
 } pcdm_variant;
 
+/* Doubly uniform samplings (tbl:ESO PAPER.md:324-355).  A run
+ * draws one realisation S_k per iteration; its slot array has tau entries, -1 for
+ * an idle processor (one that updates nothing this iteration).
+ *   NICE         tau-nice: S_k uniform over tau-subsets -- the
+ *                north_star sampling; rule: DESIGN.md R1.
+ *   INDEPENDENT  tau-independent: tau processors pick a block each, uniformly and
+ *                independently; a block picked twice is updated once (lowest
+ *                processor), the others idle (R16).
+ *   BINOMIAL     (tau, p_b)-binomial, Case 2 of PAPER.md:452-455: a tau-nice
+ *                assignment, each processor available with probability p_b
+ *                (R17; exponent reading R13).
+ *   DU           general doubly uniform with size law q[0..tau] (eq:p(S),
+ *                PAPER.md:418-422): |S_k| = K ~ q, S_k = the first K slots of the
+ *                tau-nice slot array (needs 2 tau <= n; R18).
+ * beta for every kind: thm:ESO-DU,
+ *   beta = 1 + (omega-1)(E|S|^2/E|S| - 1)/max(1,n-1)  (= thm:ESO-nice for NICE). */
+typedef enum {
+    PCDM_SAMPLING_NICE = 0,
+    PCDM_SAMPLING_INDEPENDENT = 1,
+    PCDM_SAMPLING_BINOMIAL = 2,
+    PCDM_SAMPLING_DU = 3
+} pcdm_sampling_kind;
+
+typedef struct {
+    int32_t kind;      /* pcdm_sampling_kind                                      */
+    int32_t reserved;  /* 0                                                       */
+    int64_t tau;       /* processors / slots per iteration, 1 <= tau <= n          */
+    double p_b;        /* BINOMIAL: availability probability, 0 < p_b <= 1        */
+    const double *q;   /* DU: host array q[0..tau], q_k = P(|S| = k), sums to 1
+                          (|sum - 1| <= 1e-9); borrowed for the call              */
+} pcdm_sampling;
+
 typedef struct {
     int64_t iters;              /* iterations executed by the last run              */
     int64_t nonzero_deltas;     /* number of (i in S_k, k) with delta_i != 0        */
@@ -133,6 +165,17 @@ PCDM_API pcdm_status pcdm_run_ex(pcdm_problem *p, float *x, int64_t tau, int64_t
                         int64_t first_iter, int64_t refresh_every, double beta_override,
                         int32_t variant, void *stream);
 
+/* pcdm_run_ex with any doubly uniform sampling (pcdm_sampling above).  Same
+ * arguments and errors as pcdm_run_ex, plus EINVAL for an invalid sampling (unknown
+ * kind, tau not in [1,n], p_b not in (0,1], q NULL / negative / not summing to 1,
+ * DU with 2 tau > n).  The default refresh period uses R = ceil(2n / tau). */
+PCDM_API pcdm_status pcdm_run_sampling(pcdm_problem *p, float *x, const pcdm_sampling *sampling, int64_t iters,
+                              uint64_t seed, int64_t first_iter, int64_t refresh_every, double beta_override,
+                              int32_t variant, void *stream);
+
+/* beta of thm:ESO-DU for `sampling` on this problem (fp64, host). */
+PCDM_API pcdm_status pcdm_beta_sampling(const pcdm_problem *p, const pcdm_sampling *sampling, double *beta);
+
 /* F(x) = 1/2||Ax-b||^2 + lambda||x||_1, residual accumulated in fp64 from scratch,
  * sums in fp64 (eq:P). x float32[n] host or device. Synchronises `stream`. */
 PCDM_API pcdm_status pcdm_objective(pcdm_problem *p, const float *x, double *F, void *stream);
@@ -146,6 +189,10 @@ PCDM_API pcdm_status pcdm_last_run_stats(const pcdm_problem *p, pcdm_run_stats *
  * row-major by k), exactly as pcdm_run draws them.  1 <= tau <= n < 2^31. */
 PCDM_API pcdm_status pcdm_sample(int64_t n, int64_t tau, uint64_t seed, int64_t first_iter, int64_t count,
                         int32_t *slots, void *stream);
+
+/* pcdm_sample for any sampling: slot arrays int32[count*tau], -1 = idle slot. */
+PCDM_API pcdm_status pcdm_sample_sampling(int64_t n, const pcdm_sampling *sampling, uint64_t seed, int64_t first_iter,
+                                 int64_t count, int32_t *slots, void *stream);
 
 /* L_i = ||a_i||^2 as stored by the library (float32[n]). */
 PCDM_API pcdm_status pcdm_col_norms(const pcdm_problem *p, float *L, void *stream);

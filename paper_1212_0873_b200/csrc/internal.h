@@ -26,7 +26,16 @@ cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t 
 cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
                                   cudaStream_t st, int sms, int64_t* launches);
 
-// ---- tau-nice sampler (kernels_sampler.cu)
+// ---- samplers (kernels_sampler.cu)
+// Doubly uniform samplings of PAPER.md:418-456 (pcdm_sampling_kind); the slot
+// arrays hold tau entries per iteration, -1 for an idle processor.
+struct SamplingDev {
+    int kind;                  // 0 nice, 1 independent, 2 binomial, 3 du
+    uint64_t thin_T;           // binomial: processor available iff word < thin_T ...
+    int thin_always;           // ... or always (p_b >= 1)
+    const uint64_t* du_T;      // du: device thresholds floor(cum_s 2^64), s < tau
+    int64_t du_always_from;    // du: first s with cum_s >= 1 (tau if none)
+};
 struct SamplerWork {
     int64_t n, tau, cnt;        // cnt = slots drawn per iteration (tau or n - tau)
     bool complement;            // 2 tau > n: draw the n - tau excluded values
@@ -40,9 +49,9 @@ struct SamplerWork {
     int* rounds_max;            // device scalar
 };
 // Fill slots[it * tau + j] for it in [0, count), iterations k = k0 + it.
-cudaError_t sample_chunk(const SamplerWork& w, uint64_t seed, int64_t k0, int64_t count, int* slots,
-                         int* flags, cudaStream_t st, int sms, int64_t* launches);
-size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out);
+cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t seed, int64_t k0, int64_t count,
+                         int* slots, int* flags, cudaStream_t st, int sms, int64_t* launches);
+size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out, bool no_complement = false);
 
 cudaError_t launch_philox(int64_t count, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
                           cudaStream_t st);

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kGridThreads) pcdm_iter_kernel(IterParams P) {
         // ---------------- phase A: gathers from the snapshot r_k
         for (int64_t j = gid; j < tau; j += ngroups) {
             const int i = ld_stream_s32(S + j);
+            if (i < 0) continue;  // idle processor (non-nice samplings)
             const long long s = ld_stream_s64((const long long*)P.colptr + i);
             const long long e = ld_stream_s64((const long long*)P.colptr + i + 1);
             float acc = 0.0f;
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
         const int* S = P.slots + it * tau;
         for (int j = gid; j < tau; j += ngroups) {
             const int i = S[j];
+            if (i < 0) continue;  // idle processor
             const int s = s_col[i], e = s_col[i + 1];
             float acc = 0.0f;
             for (int base = s; base < e; base += G) {

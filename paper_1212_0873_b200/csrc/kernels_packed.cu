@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
         // ---------------- phase A: one coalesced block load + <= 2 gathers per lane
         for (int64_t j = gid; j < tau; j += ngroups) {
             const int i = ld_stream_s32(S + j);
+            if (i < 0) continue;  // idle processor (non-nice samplings)
             float xi = 0.0f;
             if (t == 0) xi = ld_l2_f32(P.x + i);
             const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);

@@ -105,6 +105,79 @@ __global__ void sample_rounds_kernel(DrawArgs a, int64_t k0, unsigned long long*
     if (threadIdx.x == 0) atomicMax(rounds_max, (int)rho);
 }
 
+// ---------------------------------------------------------------- other DU samplings
+// 64-bit word of counter (j, k, 0, tag) (the same Philox stream as the draws).
+__device__ __forceinline__ uint64_t sampler_word(uint64_t seed, uint32_t k, uint32_t j, uint32_t tag) {
+    u32x4 o = philox4x32_10(u32x4{j, k, 0u, tag}, (uint32_t)seed, (uint32_t)(seed >> 32));
+    return ((uint64_t)o.y << 32) | (uint64_t)o.x;
+}
+
+// tau-independent (R16): processor j picks the first
+// accepted draw of counters (j, k, rho, tag 3); the lowest j keeps a shared pick.
+__global__ void sample_indep_insert_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables,
+                                           int* slots) {
+    const int64_t total = count * a.cnt;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t it = t / a.cnt;
+        const uint32_t j = (uint32_t)(t - it * a.cnt);
+        long long v;
+        uint32_t rho = 0;
+        while ((v = draw_value(a.seed, (uint32_t)(k0 + it), rho, j, 3u, a.n, a.reject_below)) < 0) ++rho;
+        slots[t] = (int)v;
+        table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+    }
+}
+
+__global__ void sample_indep_check_kernel(DrawArgs a, int64_t count, const unsigned long long* tables, int* slots) {
+    const int64_t total = count * a.cnt;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t it = t / a.cnt;
+        const uint32_t j = (uint32_t)(t - it * a.cnt);
+        const int v = slots[t];
+        if (table_owner(tables + (it << a.log2h), a.log2h, (uint32_t)v) != j) slots[t] = -1;
+    }
+}
+
+// (tau, p_b)-binomial, Case 2 of PAPER.md:452-455 (R17): processor j of
+// the tau-nice assignment is available iff word(j, k, 0, tag 4) < T.
+__global__ void sample_thin_kernel(uint64_t seed, int64_t k0, int64_t count, int64_t tau, uint64_t T, int* slots) {
+    const int64_t total = count * tau;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t it = t / tau;
+        const uint32_t j = (uint32_t)(t - it * tau);
+        if (!(sampler_word(seed, (uint32_t)(k0 + it), j, 4u) < T)) slots[t] = -1;
+    }
+}
+
+// DU(q) (eq:p(S); R18): K = first s with u < T[s]
+// (or s >= always_from), u = word(0, k, 0, tag 5); slots j >= K are idle.
+__global__ void sample_du_size_kernel(uint64_t seed, int64_t k0, int64_t count, int64_t tau, const uint64_t* T,
+                                      int64_t always_from, int* K) {
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < count;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = sampler_word(seed, (uint32_t)(k0 + it), 0u, 5u);
+        int64_t lo = 0, hi = tau;  // first s in [0, tau) with the predicate, else tau
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (mid >= always_from || u < T[mid]) hi = mid;
+            else lo = mid + 1;
+        }
+        K[it] = (int)lo;
+    }
+}
+
+__global__ void sample_du_mask_kernel(int64_t count, int64_t tau, const int* K, int* slots) {
+    const int64_t total = count * tau;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t it = t / tau;
+        if (t - it * tau >= K[it]) slots[t] = -1;
+    }
+}
+
 // Complement: S_k = [n] minus the owned (excluded) values, ascending.
 constexpr int kScanThreads = 512;
 __global__ void __launch_bounds__(kScanThreads) sample_complement_kernel(int64_t n, int64_t tau, int64_t cnt,
@@ -172,8 +245,8 @@ inline int blocks_for(int64_t work, int threads, int max_blocks) {
 
 namespace pcdm_internal {
 
-size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out) {
-    const bool comp = 2 * tau > n;
+size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out, bool no_complement) {
+    const bool comp = 2 * tau > n && !no_complement;
     const int64_t cnt = comp ? n - tau : tau;
     int log2h = 0;
     while ((int64_t(1) << log2h) < 2 * cnt) ++log2h;
@@ -183,8 +256,8 @@ size_t sampler_bytes_per_iter(int64_t n, int64_t tau, int* log2h_out) {
     return bytes;
 }
 
-cudaError_t sample_chunk(const SamplerWork& w, uint64_t seed, int64_t k0, int64_t count, int* slots,
-                         int* flags, cudaStream_t st, int sms, int64_t* launches) {
+cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t seed, int64_t k0, int64_t count,
+                         int* slots, int* flags, cudaStream_t st, int sms, int64_t* launches) {
     cudaError_t e;
     DrawArgs a;
     a.seed = seed;
@@ -193,13 +266,21 @@ cudaError_t sample_chunk(const SamplerWork& w, uint64_t seed, int64_t k0, int64_
     a.tag = w.complement ? 2u : 1u;
     a.cnt = w.cnt;
     a.log2h = w.log2h;
+    const int blocks = blocks_for(count * w.cnt, 256, sms * 8);
+    if (sd.kind == 1) {  // tau-independent: one ownership pass, no redraws of collisions
+        e = cudaMemsetAsync(w.tables, 0xFF, (size_t)count * ((size_t)1 << w.log2h) * 8, st);
+        if (e != cudaSuccess) return e;
+        sample_indep_insert_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, slots);
+        sample_indep_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, slots);
+        *launches += 2;
+        return cudaGetLastError();
+    }
     int* cand = w.complement ? w.cand : slots;
     if (w.cnt > 0) {
         e = cudaMemsetAsync(w.tables, 0xFF, (size_t)count * ((size_t)1 << w.log2h) * 8, st);
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(w.npending, 0, (size_t)count * sizeof(int), st);
         if (e != cudaSuccess) return e;
-        const int blocks = blocks_for(count * w.cnt, 256, sms * 8);
         sample_round0_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
         sample_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
         sample_rounds_kernel<<<(unsigned)count, 256, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
@@ -214,6 +295,19 @@ cudaError_t sample_chunk(const SamplerWork& w, uint64_t seed, int64_t k0, int64_
         sample_complement_kernel<<<(unsigned)count, kScanThreads, 0, st>>>(w.n, w.tau, w.cnt, w.cand, w.marks,
                                                                           slots);
         ++*launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const int tblocks = blocks_for(count * w.tau, 256, sms * 8);
+    if (sd.kind == 2 && !sd.thin_always) {
+        sample_thin_kernel<<<tblocks, 256, 0, st>>>(seed, k0, count, w.tau, sd.thin_T, slots);
+        ++*launches;
+        e = cudaGetLastError();
+    } else if (sd.kind == 3) {
+        sample_du_size_kernel<<<blocks_for(count, 128, sms), 128, 0, st>>>(seed, k0, count, w.tau, sd.du_T,
+                                                                           sd.du_always_from, w.npending);
+        sample_du_mask_kernel<<<tblocks, 256, 0, st>>>(count, w.tau, w.npending, slots);
+        *launches += 2;
         e = cudaGetLastError();
     }
     return e;

@@ -4,6 +4,7 @@
 // create-time kernels, and runs the PCDM1 loop as alternating sampler passes
 // and persistent iteration-kernel launches on the caller's stream.
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -93,6 +94,8 @@ struct pcdm_problem {
     int64_t nz_cap = 0;
     void* samp_mem = nullptr;
     size_t samp_cap = 0;
+    uint64_t* du_T = nullptr;  // DU-sampling thresholds
+    size_t du_cap = 0;
     pcdm_run_stats stats{};
     std::vector<cudaEvent_t> events;  // timing events, reused across runs
     DevCSC csc() const { return DevCSC{m, n, nnz, colptr, rowidx, val}; }
@@ -123,6 +126,7 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->nz_idx);
     cudaFree(p->nz_delta);
     cudaFree(p->samp_mem);
+    cudaFree(p->du_T);
     for (cudaEvent_t e : p->events) cudaEventDestroy(e);
     delete p;
 }
@@ -198,10 +202,11 @@ struct SamplerPlan {
 };
 
 // Carve the sampler + slot workspace for `chunk` iterations out of p->samp_mem.
-pcdm_status sampler_workspace(void** mem, size_t* cap, int64_t n, int64_t tau, int64_t chunk, SamplerPlan* sp) {
+pcdm_status sampler_workspace(void** mem, size_t* cap, int64_t n, int64_t tau, int64_t chunk, SamplerPlan* sp,
+                              bool no_complement = false) {
     int log2h = 0;
-    sampler_bytes_per_iter(n, tau, &log2h);
-    const bool comp = 2 * tau > n;
+    sampler_bytes_per_iter(n, tau, &log2h, no_complement);
+    const bool comp = 2 * tau > n && !no_complement;
     const int64_t cnt = comp ? n - tau : tau;
     auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
     size_t off = 0;
@@ -247,6 +252,129 @@ int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
     if (const char* fc = getenv("PCDM_CHUNK")) c = std::max<int64_t>(1, atoll(fc));  // tests / tuning
     return std::min<int64_t>(c, std::max<int64_t>(iters, 1));
 }
+
+// A sampling of the run (pcdm_sampling, validated) plus what the device needs.
+struct SamplingSpec {
+    int kind = PCDM_SAMPLING_NICE;
+    int64_t tau = 1;
+    double p_b = 1.0;
+    std::vector<double> q;
+};
+
+pcdm_status check_sampling(const pcdm_sampling* sp, int64_t n, SamplingSpec* out) {
+    if (!sp) return fail(PCDM_EINVAL, "NULL sampling");
+    out->kind = sp->kind;
+    out->tau = sp->tau;
+    out->p_b = sp->p_b;
+    if (sp->kind < PCDM_SAMPLING_NICE || sp->kind > PCDM_SAMPLING_DU) return fail(PCDM_EINVAL, "unknown sampling kind %d", sp->kind);
+    if (sp->tau < 1 || sp->tau > n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
+    if (sp->kind == PCDM_SAMPLING_BINOMIAL && !(sp->p_b > 0.0 && sp->p_b <= 1.0))
+        return fail(PCDM_EINVAL, "binomial sampling needs 0 < p_b <= 1");
+    if (sp->kind == PCDM_SAMPLING_DU) {
+        if (!sp->q) return fail(PCDM_EINVAL, "DU sampling needs q[0..tau]");
+        if (2 * sp->tau > n) return fail(PCDM_EINVAL, "DU sampling needs 2 tau <= n");
+        double sum = 0.0;
+        out->q.assign(sp->q, sp->q + sp->tau + 1);
+        for (double v : out->q) {
+            if (!(v >= 0.0 && v <= 1.0)) return fail(PCDM_EINVAL, "q entries must be in [0, 1]");
+            sum += v;
+        }
+        if (!(fabs(sum - 1.0) <= 1e-9)) return fail(PCDM_EINVAL, "q must sum to 1 (sum %.17g)", sum);
+    }
+    return PCDM_OK;
+}
+
+// (E|S|, E|S|^2) of the sampling (thm:ESO-DU inputs):
+//   nice tau, tau^2; binomial tau p_b, tau p_b (1 + tau p_b - p_b);
+//   DU sum k q_k, sum k^2 q_k; tau-independent = occupied bins of tau balls in n
+//   bins: E|S| = n(1 - a), E|S|^2 = E|S| + n(n-1)(1 - 2a + b), a = (1-1/n)^tau,
+//   b = (1-2/n)^tau, evaluated through expm1/log1p (1-2a+b = 2(1-a) - (1-b)).
+void sampling_moments(const SamplingSpec& sp, int64_t n, double* e1, double* e2) {
+    const double t = (double)sp.tau, nn = (double)n;
+    switch (sp.kind) {
+        case PCDM_SAMPLING_INDEPENDENT: {
+            const double one_minus_a = -expm1(t * log1p(-1.0 / nn));
+            const double one_minus_b = n >= 2 ? -expm1(t * log1p(-2.0 / nn)) : 1.0;
+            *e1 = nn * one_minus_a;
+            *e2 = *e1 + nn * (nn - 1.0) * (2.0 * one_minus_a - one_minus_b);
+            return;
+        }
+        case PCDM_SAMPLING_BINOMIAL:
+            *e1 = t * sp.p_b;
+            *e2 = t * sp.p_b * (1.0 + t * sp.p_b - sp.p_b);
+            return;
+        case PCDM_SAMPLING_DU: {
+            double a1 = 0.0, a2 = 0.0;
+            for (size_t k = 0; k < sp.q.size(); ++k) {
+                a1 += (double)k * sp.q[k];
+                a2 += (double)k * (double)k * sp.q[k];
+            }
+            *e1 = a1;
+            *e2 = a2;
+            return;
+        }
+        default:
+            *e1 = t;
+            *e2 = t * t;
+    }
+}
+
+// beta = 1 + (omega-1)(E|S|^2/E|S| - 1)/max(1,n-1)  (thm:ESO-DU)
+double sampling_beta(const SamplingSpec& sp, int64_t omega, int64_t n) {
+    if (sp.kind == PCDM_SAMPLING_NICE) {  // the north_star form, thm:ESO-nice
+        const double denom = (double)std::max<int64_t>(1, n - 1);
+        return 1.0 + (double)(omega - 1) * (double)(sp.tau - 1) / denom;
+    }
+    double e1, e2;
+    sampling_moments(sp, n, &e1, &e2);
+    if (!(e1 > 0.0)) return 1.0;
+    return 1.0 + (double)(omega - 1) * (e2 / e1 - 1.0) / (double)std::max<int64_t>(1, n - 1);
+}
+
+// floor(p 2^64) (p < 1) or "always" (p >= 1), exactly as the oracle's reading R17/R18
+uint64_t prob_threshold(double p, int* always) {
+    *always = 0;
+    if (p >= 1.0) {
+        *always = 1;
+        return ~0ull;
+    }
+    if (p <= 0.0) return 0;
+    return (uint64_t)(p * 18446744073709551616.0);
+}
+
+// Device-side description; DU thresholds go to `dev_T` (tau entries).
+pcdm_status sampling_dev(const SamplingSpec& sp, uint64_t** dev_T, size_t* cap, cudaStream_t st, SamplingDev* out) {
+    out->kind = sp.kind;
+    out->thin_T = 0;
+    out->thin_always = 1;
+    out->du_T = nullptr;
+    out->du_always_from = sp.tau;
+    if (sp.kind == PCDM_SAMPLING_BINOMIAL) out->thin_T = prob_threshold(sp.p_b, &out->thin_always);
+    if (sp.kind == PCDM_SAMPLING_DU) {
+        std::vector<uint64_t> T((size_t)sp.tau);
+        double cum = 0.0;
+        for (int64_t s = 0; s < sp.tau; ++s) {
+            cum += sp.q[(size_t)s];
+            int always = 0;
+            T[(size_t)s] = prob_threshold(cum, &always);
+            if (always && out->du_always_from == sp.tau) out->du_always_from = s;
+        }
+        if (*cap < T.size()) {
+            cudaFree(*dev_T);
+            *dev_T = nullptr;
+            *cap = 0;
+            CK(cudaMalloc((void**)dev_T, sizeof(uint64_t) * T.size()), "DU thresholds");
+            *cap = T.size();
+        }
+        CK(cudaMemcpyAsync(*dev_T, T.data(), sizeof(uint64_t) * T.size(), cudaMemcpyHostToDevice, st), "DU thresholds");
+        CK(cudaStreamSynchronize(st), "DU thresholds");  // T is a stack vector
+        out->du_T = *dev_T;
+    }
+    return PCDM_OK;
+}
+
+pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_t iters, uint64_t seed,
+                     int64_t first_iter, int64_t refresh_every, double beta_override, int32_t variant, void* stream);
 
 }  // namespace
 
@@ -354,7 +482,30 @@ pcdm_status pcdm_run(pcdm_problem* p, float* x, int64_t tau, int64_t iters, uint
 pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, uint64_t seed, int64_t first_iter,
                         int64_t refresh_every, double beta_override, int32_t variant, void* stream) {
     if (!p || !x) return fail(PCDM_EINVAL, "NULL argument");
-    if (tau < 1 || tau > p->n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
+    pcdm_sampling smp{};
+    smp.kind = PCDM_SAMPLING_NICE;
+    smp.tau = tau;
+    smp.p_b = 1.0;
+    return pcdm_run_sampling(p, x, &smp, iters, seed, first_iter, refresh_every, beta_override, variant, stream);
+}
+
+pcdm_status pcdm_run_sampling(pcdm_problem* p, float* x, const pcdm_sampling* sampling, int64_t iters, uint64_t seed,
+                              int64_t first_iter, int64_t refresh_every, double beta_override, int32_t variant,
+                              void* stream) {
+    if (!p || !x) return fail(PCDM_EINVAL, "NULL argument");
+    SamplingSpec spec;
+    pcdm_status s0 = check_sampling(sampling, p->n, &spec);
+    if (s0 != PCDM_OK) return s0;
+    return run_impl(p, x, spec, iters, seed, first_iter, refresh_every, beta_override, variant, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_t iters, uint64_t seed,
+                     int64_t first_iter, int64_t refresh_every, double beta_override, int32_t variant, void* stream) {
+    const int64_t tau = spec.tau;
     if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
     if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
     if (variant < 0 || variant > 4) return fail(PCDM_EINVAL, "unknown variant %d", variant);
@@ -385,8 +536,7 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
     if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
     if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
 
-    double beta_d;
-    pcdm_beta(p, tau, &beta_d);
+    double beta_d = sampling_beta(spec, p->omega, p->n);
     if (beta_override > 0.0) beta_d = beta_override;
     const int64_t R = refresh_period(p->n, tau, refresh_every);
     IterLaunch plan = plan_iter(variant == PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
@@ -421,8 +571,12 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
     int64_t chunk = choose_chunk(p->n, tau, iters);
     if (R > 0) chunk = std::min(chunk, R);
     SamplerPlan sp;
-    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, chunk, &sp)) != PCDM_OK) return s;
+    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, chunk, &sp,
+                               spec.kind == PCDM_SAMPLING_INDEPENDENT)) != PCDM_OK)
+        return s;
     CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), st), "memset rounds");
+    SamplingDev sdev;
+    if ((s = sampling_dev(spec, &p->du_T, &p->du_cap, st, &sdev)) != PCDM_OK) return s;
 
     IterParams P{};
     P.colptr = p->colptr;
@@ -463,7 +617,7 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
         if (R > 0) c = std::min(c, R - (done % R));
         int ts;
         CK(tm.begin(&ts), "event");
-        CK(sample_chunk(sp.w, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
+        CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
            "sampler");
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
@@ -526,6 +680,10 @@ pcdm_status pcdm_run_ex(pcdm_problem* p, float* x, int64_t tau, int64_t iters, u
     return PCDM_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 pcdm_status pcdm_objective(pcdm_problem* p, const float* x, double* F, void* stream) {
     if (!p || !x || !F) return fail(PCDM_EINVAL, "NULL argument");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
@@ -562,9 +720,21 @@ pcdm_status pcdm_last_run_stats(const pcdm_problem* p, pcdm_run_stats* stats) {
 
 pcdm_status pcdm_sample(int64_t n, int64_t tau, uint64_t seed, int64_t first_iter, int64_t count, int32_t* slots,
                         void* stream) {
+    pcdm_sampling smp{};
+    smp.kind = PCDM_SAMPLING_NICE;
+    smp.tau = tau;
+    smp.p_b = 1.0;
+    return pcdm_sample_sampling(n, &smp, seed, first_iter, count, slots, stream);
+}
+
+pcdm_status pcdm_sample_sampling(int64_t n, const pcdm_sampling* sampling, uint64_t seed, int64_t first_iter,
+                                 int64_t count, int32_t* slots, void* stream) {
     if (!slots) return fail(PCDM_EINVAL, "NULL argument");
     if (n < 1 || n >= (1ll << 31)) return fail(PCDM_EINVAL, "n must be in [1, 2^31)");
-    if (tau < 1 || tau > n) return fail(PCDM_EINVAL, "tau must be in [1, n]");
+    SamplingSpec spec;
+    pcdm_status s = check_sampling(sampling, n, &spec);
+    if (s != PCDM_OK) return s;
+    const int64_t tau = spec.tau;
     if (count < 0 || first_iter < 0 || first_iter + count > (1ll << 32))
         return fail(PCDM_EINVAL, "bad iteration range");
     if (count == 0) return PCDM_OK;
@@ -576,16 +746,24 @@ pcdm_status pcdm_sample(int64_t n, int64_t tau, uint64_t seed, int64_t first_ite
     void* mem = nullptr;
     size_t cap = 0;
     int* flags = nullptr;
+    uint64_t* dT = nullptr;
+    size_t dcap = 0;
     SamplerPlan sp;
-    pcdm_status s = sampler_workspace(&mem, &cap, n, tau, chunk, &sp);
-    if (s != PCDM_OK) return s;
+    SamplingDev sdev;
+    s = sampler_workspace(&mem, &cap, n, tau, chunk, &sp, spec.kind == PCDM_SAMPLING_INDEPENDENT);
+    if (s == PCDM_OK) s = sampling_dev(spec, &dT, &dcap, st, &sdev);
+    if (s != PCDM_OK) {
+        cudaFree(mem);
+        cudaFree(dT);
+        return s;
+    }
     int64_t launches = 0;
     cudaError_t e = cudaMalloc((void**)&flags, sizeof(int));
     if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(int), st);
     const bool dev_out = is_device_ptr(slots);
     for (int64_t done = 0; e == cudaSuccess && done < count;) {
         const int64_t c = std::min(chunk, count - done);
-        e = sample_chunk(sp.w, seed, first_iter + done, c, sp.slots, flags, st, sms, &launches);
+        e = sample_chunk(sp.w, sdev, seed, first_iter + done, c, sp.slots, flags, st, sms, &launches);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(slots + done * tau, sp.slots, sizeof(int) * c * tau,
                                 dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st);
@@ -596,8 +774,18 @@ pcdm_status pcdm_sample(int64_t n, int64_t tau, uint64_t seed, int64_t first_ite
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(mem);
     cudaFree(flags);
+    cudaFree(dT);
     if (e != cudaSuccess) return cuda_fail(e, "pcdm_sample");
     if (hflags & FLAG_SAMPLER) return fail(PCDM_ESAMPLER, "sampler round counter overflow");
+    return PCDM_OK;
+}
+
+pcdm_status pcdm_beta_sampling(const pcdm_problem* p, const pcdm_sampling* sampling, double* beta) {
+    if (!p || !beta) return fail(PCDM_EINVAL, "NULL argument");
+    SamplingSpec spec;
+    pcdm_status s = check_sampling(sampling, p->n, &spec);
+    if (s != PCDM_OK) return s;
+    *beta = sampling_beta(spec, p->omega, p->n);
     return PCDM_OK;
 }
 

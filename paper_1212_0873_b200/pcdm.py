@@ -22,7 +22,9 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EDIVERGED", 5
 
 EXPORTS = ["pcdm_create", "pcdm_destroy", "pcdm_last_error", "pcdm_omega", "pcdm_beta", "pcdm_run",
            "pcdm_run_ex", "pcdm_objective", "pcdm_last_run_stats", "pcdm_sample", "pcdm_col_norms",
-           "pcdm_row_counts", "pcdm_residual", "pcdm_philox", "pcdm_philox_check_curand"]
+           "pcdm_row_counts", "pcdm_residual", "pcdm_philox", "pcdm_philox_check_curand",
+           "pcdm_run_sampling", "pcdm_beta_sampling", "pcdm_sample_sampling"]
+SAMPLING_KINDS = {"nice": 0, "independent": 1, "binomial": 2, "du": 3}
 
 
 class PCDMError(RuntimeError):
@@ -43,6 +45,26 @@ class RunStats(ctypes.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class _CSampling(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32), ("tau", ctypes.c_int64),
+                ("p_b", ctypes.c_double), ("q", ctypes.c_void_p)]
+
+
+class Sampling:
+    """A doubly uniform sampling for pcdm_run_sampling (include/pcdm.h): kind in
+    SAMPLING_KINDS, tau slots, p_b (binomial), q[0..tau] (du)."""
+
+    def __init__(self, kind="nice", tau=1, p_b=1.0, q=None):
+        if kind not in SAMPLING_KINDS:
+            raise ValueError("unknown sampling kind %r" % kind)
+        self.kind, self.tau, self.p_b = kind, int(tau), float(p_b)
+        self.q = None if q is None else np.ascontiguousarray(q, dtype=np.float64)
+
+    def c(self):
+        return _CSampling(SAMPLING_KINDS[self.kind], 0, self.tau, self.p_b,
+                          None if self.q is None else self.q.ctypes.data)
 
 
 _lib = None
@@ -75,6 +97,9 @@ def load():
         "pcdm_residual": ([P, P, P], st),
         "pcdm_philox": ([i64, P, P, P, P], st),
         "pcdm_philox_check_curand": ([i64, u64, ctypes.POINTER(i64), P], st),
+        "pcdm_run_sampling": ([P, P, ctypes.POINTER(_CSampling), i64, u64, i64, i64, f64, i32, P], st),
+        "pcdm_beta_sampling": ([P, ctypes.POINTER(_CSampling), ctypes.POINTER(f64)], st),
+        "pcdm_sample_sampling": ([i64, ctypes.POINTER(_CSampling), u64, i64, i64, P, P], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -160,6 +185,28 @@ def pcdm_run_ex(h, x, tau, iters, seed, first_iter=0, refresh_every=0, beta_over
                               int(refresh_every), float(beta_override), v, _stream(stream)))
 
 
+def pcdm_run_sampling(h, x, sampling: Sampling, iters, seed, first_iter=0, refresh_every=0, beta_override=0.0,
+                      variant="auto", stream=None):
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    cs = sampling.c()
+    _check(load().pcdm_run_sampling(h, _ptr(x, "f32"), ctypes.byref(cs), int(iters), int(seed), int(first_iter),
+                                    int(refresh_every), float(beta_override), v, _stream(stream)))
+
+
+def pcdm_beta_sampling(h, sampling: Sampling) -> float:
+    v = ctypes.c_double()
+    cs = sampling.c()
+    _check(load().pcdm_beta_sampling(h, ctypes.byref(cs), ctypes.byref(v)))
+    return v.value
+
+
+def pcdm_sample_sampling(n, sampling: Sampling, seed, first_iter, count, out, stream=None):
+    cs = sampling.c()
+    _check(load().pcdm_sample_sampling(int(n), ctypes.byref(cs), int(seed), int(first_iter), int(count),
+                                       _ptr(out, "i32"), _stream(stream)))
+    return out
+
+
 def pcdm_objective(h, x, stream=None) -> float:
     F = ctypes.c_double()
     _check(load().pcdm_objective(h, _ptr(x, "f32"), ctypes.byref(F), _stream(stream)))
@@ -238,10 +285,18 @@ class Problem:
         return pcdm_beta(self.handle, tau)
 
     def run(self, x, tau, iters, seed=0, first_iter=0, refresh_every=0, beta_override=0.0,
-            variant="auto", stream=None):
-        pcdm_run_ex(self.handle, x, tau, iters, seed, first_iter, refresh_every, beta_override,
-                    variant, stream)
+            variant="auto", stream=None, sampling: Sampling = None):
+        """PCDM1 iterations; tau-nice unless `sampling` is given (then tau is ignored)."""
+        if sampling is None:
+            pcdm_run_ex(self.handle, x, tau, iters, seed, first_iter, refresh_every, beta_override,
+                        variant, stream)
+        else:
+            pcdm_run_sampling(self.handle, x, sampling, iters, seed, first_iter, refresh_every, beta_override,
+                              variant, stream)
         return x
+
+    def beta_sampling(self, sampling: Sampling):
+        return pcdm_beta_sampling(self.handle, sampling)
 
     def objective(self, x, stream=None):
         return pcdm_objective(self.handle, x, stream)

@@ -16,16 +16,19 @@ def to_host(t):
 
 
 def run_both(colptr, rowidx, val, b, lam, m, tau, iters, seed=0, x0=None, first_iter=0,
-             refresh_every=0, beta_override=0.0, variant="auto", device="cuda:0"):
+             refresh_every=0, beta_override=0.0, variant="auto", device="cuda:0", sampling=None):
     """Run the CUDA path (device x) and the oracle on the same arrays.
+    sampling: None (tau-nice) or a spec (kind, tau, p_b, q) handed to both sides.
     Returns dict with x_gpu, x_orc (fp64), F_gpu (library objective), F_orc, stats, res."""
     n = colptr.numel() - 1
     dev = torch.device(device)
     prob = pcdm.Problem(m, n, colptr.to(dev), rowidx.to(dev), val.to(dev), b.to(dev), lam)
     x = torch.zeros(n, dtype=torch.float32, device=dev) if x0 is None else \
         torch.as_tensor(x0, dtype=torch.float32).to(dev).clone()
+    gs = None if sampling is None else pcdm.Sampling(*sampling)
     prob.run(x, tau, iters, seed=seed, first_iter=first_iter, refresh_every=refresh_every,
-             beta_override=beta_override, variant=variant)
+             beta_override=beta_override, variant=variant, sampling=gs)
+    beta_gpu = prob.beta(tau) if gs is None else prob.beta_sampling(gs)
     torch.cuda.synchronize()
     stats = prob.stats()
     F_gpu = prob.objective(x)
@@ -37,10 +40,11 @@ def run_both(colptr, rowidx, val, b, lam, m, tau, iters, seed=0, x0=None, first_
     x0h = None if x0 is None else np.asarray(to_host(torch.as_tensor(x0)), dtype=np.float32).astype(np.float64)
     res = oracle.run(m, c, r, v, bb, lam, tau, iters, seed, x0=x0h, first_iter=first_iter,
                      refresh_every=refresh_every,
-                     beta_override=beta_override if beta_override > 0 else None)
+                     beta_override=beta_override if beta_override > 0 else None,
+                     sampling=None if sampling is None else oracle.Sampling(*sampling))
     F_orc = oracle.objective(m, c, r, v, bb, lam, res.x)
     return dict(x_gpu=to_host(x).astype(np.float64), x_orc=res.x, F_gpu=F_gpu, F_orc=F_orc,
-                stats=stats, res=res, r_gpu=to_host(r_gpu), omega_gpu=omega_gpu)
+                stats=stats, res=res, r_gpu=to_host(r_gpu), omega_gpu=omega_gpu, beta_gpu=beta_gpu)
 
 
 def assert_parity(out, f_rtol=F_RTOL, x_rtol=X_RTOL):

@@ -288,3 +288,51 @@ def test_many_chunks_per_run(gpu, monkeypatch, variant):
         out = run_both(c, r, v, b, lam, 3000, tau, iters, seed=5, variant=variant, refresh_every=refresh)
         assert_parity(out)
         assert out["stats"]["iter_launches"] >= iters // 3
+
+
+# ------------------------------------------------------------------ other DU samplings (NEXT-1)
+SAMPLINGS = [("independent", 37, 1.0, None), ("independent", 700, 1.0, None), ("binomial", 64, 0.3, None),
+             ("binomial", 700, 0.75, None), ("binomial", 500, 1.0, None),
+             ("du", 40, 1.0, list(np.random.default_rng(9).dirichlet(np.ones(41))))]
+
+
+@pytest.mark.parametrize("spec", SAMPLINGS, ids=lambda s: "%s-%d" % (s[0], s[1]))
+def test_sampling_slot_arrays_bitexact(gpu, spec):
+    n = 700
+    count = 12
+    got = np.zeros(count * spec[1], dtype=np.int32)
+    pcdm.pcdm_sample_sampling(n, pcdm.Sampling(*spec), 5, 3, count, got, stream=0)
+    got = got.reshape(count, spec[1])
+    osp = oracle.Sampling(*spec)
+    for k in range(count):
+        assert np.array_equal(got[k], oracle.sample_kind(osp, 5, 3 + k, n)), k
+    # huge-shaped independent / binomial draws too
+    for spec2 in (("independent", 1 << 16, 1.0, None), ("binomial", 1 << 16, 0.5, None)):
+        g = torch.zeros(2 << 16, dtype=torch.int32, device=gpu)
+        pcdm.pcdm_sample_sampling(500_000_000, pcdm.Sampling(*spec2), 1, 0, 2, g)
+        g = to_host(g).reshape(2, -1)
+        for k in range(2):
+            assert np.array_equal(g[k], oracle.sample_kind(oracle.Sampling(*spec2), 1, k, 500_000_000))
+
+
+@pytest.mark.parametrize("spec", SAMPLINGS, ids=lambda s: "%s-%d" % (s[0], s[1]))
+@pytest.mark.parametrize("variant", ["packed", "grid", "smem"])
+def test_sampling_runs_match_oracle(gpu, spec, variant):
+    m, n = 900, 700
+    c, r, v, b, lam = _ragged(m, n, np.random.default_rng(2).integers(1, 30, size=n), 31)
+    out = run_both(c, r, v, b, lam, m, spec[1], 120, seed=4, variant=variant, sampling=spec)
+    assert_parity(out)
+    assert out["beta_gpu"] == pytest.approx(out["res"].beta, rel=1e-12)
+
+
+def test_sampling_errors(gpu):
+    c, r, v, b, lam = _ragged(50, 40, np.full(40, 3), 1)
+    prob = pcdm.Problem(50, 40, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), lam)
+    x = torch.zeros(40, device=gpu)
+    for bad in (pcdm.Sampling("binomial", 8, p_b=0.0), pcdm.Sampling("binomial", 8, p_b=1.5),
+                pcdm.Sampling("du", 4, q=[0.5, 0.5, 0.5, 0.0, 0.0]), pcdm.Sampling("du", 30, q=np.full(31, 1 / 31)),
+                pcdm.Sampling("independent", 41)):
+        with pytest.raises(pcdm.PCDMError) as e:
+            prob.run(x, 0, 1, sampling=bad)
+        assert e.value.status == pcdm.PCDM_EINVAL
+    prob.close()
