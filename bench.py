@@ -8,7 +8,7 @@ A "step" is one pcdm_run call of `iters` synchronous PCDM1 iterations (sampling,
 gathers a_i^T r, soft-threshold steps, residual scatter, barriers) on the
 config's synthetic instance; consecutive steps continue the same solve
 (first_iter advances), so every step is real work on resident HBM inputs.
-Metric: coordinate updates/s (= tau * iters per step), plus effective GB/s at
+Metric: coordinate updates/s (= E|S| * iters per step; E|S| = tau for tau-nice), plus effective GB/s at
 16 B per touched nonzero (val + idx + r gather + r scatter).
 
 Multi-GPU (torchrun): replicas only -- every rank solves its own
@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--tau", type=int, default=None)
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--variant", default="auto")
+    ap.add_argument("--sampling", default="nice", choices=["nice", "independent", "binomial"],
+                    help="doubly uniform sampling (NEXT-1 rows); the headline is tau-nice")
+    ap.add_argument("--p-b", type=float, default=0.5, help="binomial availability probability")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -177,14 +180,31 @@ def ncu_traffic(config, iters_per_launch):
 
 
 # ----------------------------------------------------------------------------- oracle sample
-def oracle_subinstance(inst, tau, k0, k_iters, seed):
+def expected_size(kind, tau, n, p_b):
+    """E|S| of the sampling (tau-nice: tau; binomial: tau p_b; tau-independent:
+    occupied bins of tau balls in n bins) -- used only to count coordinate updates."""
+    if kind == "binomial":
+        return tau * p_b
+    if kind == "independent":
+        return -n * np.expm1(tau * np.log1p(-1.0 / n))
+    return float(tau)
+
+
+def oracle_sampling(args, tau):
+    import oracle
+    return None if args.sampling == "nice" else oracle.Sampling(args.sampling, tau, p_b=args.p_b)
+
+
+def oracle_subinstance(inst, tau, k0, k_iters, seed, osamp=None):
     """Host CSC holding only the columns S_k0..S_{k0+K-1} touch (others empty),
     gathered from the resident instance; the slots come from the oracle's own
     sampler.  Test/baseline infrastructure: never on the product path."""
     import oracle
     n = inst.n
-    S = [oracle.sample(seed, k, tau, n) for k in range(k0, k0 + k_iters)]
+    S = [oracle.sample(seed, k, tau, n) if osamp is None else oracle.sample_kind(osamp, seed, k, n)
+         for k in range(k0, k0 + k_iters)]
     cols = np.unique(np.concatenate(S)).astype(np.int64)
+    cols = cols[cols >= 0]
     dev = inst.colptr.device
     ct = torch.from_numpy(cols).to(dev)
     starts = inst.colptr[ct]
@@ -200,12 +220,12 @@ def oracle_subinstance(inst, tau, k0, k_iters, seed):
     return full, rows, vals, inst.b.cpu().numpy()
 
 
-def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None):
+def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None, osamp=None):
     import oracle
     if sub is None:
-        sub = oracle_subinstance(inst, tau, k0, k_iters, seed)
+        sub = oracle_subinstance(inst, tau, k0, k_iters, seed, osamp)
     c, r, v, b = sub
-    res = oracle.run(inst.m, c, r, v, b, inst.lam, tau, k_iters, seed, first_iter=k0)
+    res = oracle.run(inst.m, c, r, v, b, inst.lam, tau, k_iters, seed, first_iter=k0, sampling=osamp)
     return res.loop_seconds, sub
 
 
@@ -219,20 +239,21 @@ def bench_reference(args, world, rank):
     dev = torch.device("cuda", 0)
     inst = I.generate(cfg, seed=0, device=dev)
     K, W = args.steps, args.warmup
-    sub = oracle_subinstance(inst, tau, 0, kref * (K + W), seed=0)
+    osamp = oracle_sampling(args, tau)
+    sub = oracle_subinstance(inst, tau, 0, kref * (K + W), seed=0, osamp=osamp)
     del inst.rowidx, inst.val
     secs = []
     for s in range(W + K):
-        t, _ = run_oracle_sample(inst, tau, s * kref, kref, 0, sub=sub)
+        t, _ = run_oracle_sample(inst, tau, s * kref, kref, 0, sub=sub, osamp=osamp)
         if s >= W:
             secs.append(t)
     step_s = sum(secs) / len(secs)
-    value = tau * kref / step_s
+    value = expected_size(args.sampling, tau, inst.n, args.p_b) * kref / step_s
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": 1,
             "steps": K, "warmup": W, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "nnz_per_col": cfg.nnz_per_col,
-                       "tau": tau, "iters_per_step": kref, "seed": 0,
+                       "tau": tau, "sampling": args.sampling, "iters_per_step": kref, "seed": 0,
                        "note": "serial oracle on host cores; each step = %d iterations of the same run" % kref},
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "oracle",
                              "sample": "iterations k=%d..%d of the %s run (columns they touch), O5-O8 loop only"
@@ -272,12 +293,15 @@ def bench_ours(args, world, rank, local):
     sub = None
     do_cpu = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     kcpu = CPU_BASELINE_ITERS[args.config]
+    osamp = oracle_sampling(args, tau) if do_cpu else None
     if do_cpu:
-        sub = oracle_subinstance(inst, tau, 0, kcpu, seed=0)
+        sub = oracle_subinstance(inst, tau, 0, kcpu, seed=0, osamp=osamp)
     del inst.rowidx, inst.val
     torch.cuda.empty_cache()
 
     run_seed = rank
+    gsamp = None if args.sampling == "nice" else pcdm.Sampling(args.sampling, tau, p_b=args.p_b)
+    size = expected_size(args.sampling, tau, inst.n, args.p_b)
     x = torch.zeros(inst.n, dtype=torch.float32, device=dev)
     flush = torch.empty(int(2 * l2_bytes) // 4, dtype=torch.float32, device=dev) \
         if working_set < 4 * l2_bytes else None
@@ -285,7 +309,7 @@ def bench_ours(args, world, rank, local):
 
     def one_step(xbuf):
         nonlocal step
-        prob.run(xbuf, tau, iters, seed=run_seed, first_iter=step * iters, variant=args.variant,
+        prob.run(xbuf, tau, iters, seed=run_seed, first_iter=step * iters, variant=args.variant, sampling=gsamp,
                  stream=stream)
         step += 1
 
@@ -309,7 +333,7 @@ def bench_ours(args, world, rank, local):
     barrier(world)
     clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    updates_per_step = tau * iters
+    updates_per_step = size * iters
     value, ms_per_step = job_throughput(updates_per_step, sum(step_ms) / K, world)
     F_final = prob.objective(x)
 
@@ -319,7 +343,7 @@ def bench_ours(args, world, rank, local):
     samp_ms = sum(s["sampler_ms"] for s in st_list)
     setup_ms = sum(s["setup_ms"] for s in st_list)
     iters_per_launch = K * iters / max(it_launches, 1)
-    alg_bytes_launch = BYTES_PER_NNZ * avg_c * tau * iters_per_launch
+    alg_bytes_launch = BYTES_PER_NNZ * avg_c * size * iters_per_launch
     launch_ms = it_ms / max(it_launches, 1)
     achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
     peak, peak_src = hbm_peak()
@@ -347,8 +371,8 @@ def bench_ours(args, world, rank, local):
 
     cpu = None
     if do_cpu:
-        secs, _ = run_oracle_sample(inst, tau, 0, kcpu, 0, sub=sub)
-        cpu = {"value": tau * kcpu / secs, "unit": "updates/s", "cores": 1, "kind": "oracle",
+        secs, _ = run_oracle_sample(inst, tau, 0, kcpu, 0, sub=sub, osamp=osamp)
+        cpu = {"value": size * kcpu / secs, "unit": "updates/s", "cores": 1, "kind": "oracle",
                "sample": "iterations k=0..%d of the %s run (tau=%d) on the columns they touch; "
                          "O5-O8 loop time %.2f s" % (kcpu - 1, cfg.name, tau, secs)}
 
@@ -361,6 +385,7 @@ def bench_ours(args, world, rank, local):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "nnz": nnz, "nnz_per_col": cfg.nnz_per_col,
                    "rows": cfg.rows, "tau": tau, "iters_per_step": iters, "seed_instance": 0,
+                   "sampling": args.sampling if args.sampling != "binomial" else "binomial(p_b=%g)" % args.p_b,
                    "seed_run": "rank", "parallelism": "replicas" if world > 1 else "single",
                    "l2": ("inputs larger than L2 (A %.1f GB vs L2 %.0f MB)" % (nnz * 8 / 1e9, l2_bytes / 1e6))
                    if flush is None else "L2 flushed between timed steps"},
@@ -375,8 +400,8 @@ def bench_ours(args, world, rank, local):
         "gpu_launches": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "omega": prob.omega, "beta": prob.beta(tau), "F_final": F_final,
-        "nonzero_step_frac": nz / (K * tau * iters),
+        "omega": prob.omega, "beta": prob.beta(tau) if gsamp is None else prob.beta_sampling(gsamp),
+        "F_final": F_final, "nonzero_step_frac": nz / (K * size * iters),
         "variant": VARIANT_NAMES.get(st0["variant"], "?"),
         "grid": {"ctas": st0["grid_ctas"], "threads": st0["threads_per_cta"], "lanes_per_column": st0["lanes_per_column"]},
         "setup_s": {"generate": gen_s, "create": create_s},
