@@ -392,6 +392,8 @@ def bench_ours(args, world, rank, local):
         "effective_GBps": value * avg_c * BYTES_PER_NNZ / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "traffic_GBps": traffic / (launch_ms / 1e3) / 1e9 if traffic else None,
+                     "traffic_frac": traffic / (launch_ms / 1e3) / 1e9 / peak if traffic else None,
                      "kernel": KERNEL_OF_VARIANT.get(st0["variant"], "?"), "algorithmic_bytes_per_launch": alg_bytes_launch,
                      "launch_ms": launch_ms, "iters_per_launch": iters_per_launch,
                      "share_of_step": it_ms / max(sum(step_ms), 1e-9)},
