@@ -225,3 +225,30 @@ def equal_row_01_matrix(m: int, n: int, omega: int, seed: int = 0):
     rowidx = torch.tensor([r for cl in cols for r in sorted(cl)], dtype=torch.int32)
     val = torch.ones(rowidx.numel(), dtype=torch.float32)
     return colptr, rowidx, val
+
+
+def equal_row_random_matrix(m: int, n: int, omega: int, seed: int = 0):
+    """0-1 matrix with exactly ``omega`` ones per row and k = omega*m/n ones per
+    column, rows drawn at random (the Sec. 8.2 "theory versus reality" matrices,
+    PAPER.md:1289, built on the DSO tightness construction PAPER.md:697-703):
+    rows come in k blocks of n/omega; block t splits a fresh random permutation
+    of the columns into n/omega groups of omega.  Needs n % omega == 0 and
+    m % (n/omega) == 0.  Returns a host CSC (colptr, rowidx, val)."""
+    if n % omega or m % (n // omega):
+        raise ValueError("need omega | n and (n/omega) | m")
+    g = n // omega
+    gen = torch.Generator(device="cpu")
+    gen.manual_seed(seed)
+    cols_of_row = []
+    for t in range(m // g):
+        perm = torch.randperm(n, generator=gen).view(g, omega)
+        cols_of_row.append(perm)
+    rows_cols = torch.cat(cols_of_row, 0)                      # [m, omega]
+    row_ids = torch.arange(m).repeat_interleave(omega)
+    col_ids = rows_cols.reshape(-1)
+    order = torch.argsort(col_ids * m + row_ids)
+    col_sorted, row_sorted = col_ids[order], row_ids[order]
+    counts = torch.bincount(col_sorted, minlength=n)
+    colptr = torch.zeros(n + 1, dtype=torch.int64)
+    colptr[1:] = torch.cumsum(counts, 0)
+    return colptr, row_sorted.to(torch.int32), torch.ones(m * omega, dtype=torch.float32)
