@@ -266,7 +266,10 @@ class Problem:
 
     def close(self):
         if getattr(self, "handle", None):
-            pcdm_destroy(self.handle)
+            try:
+                pcdm_destroy(self.handle)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self.handle = None
 
     __del__ = close

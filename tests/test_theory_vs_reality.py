@@ -37,7 +37,7 @@ def _oracle_counts(orc, c, r, v, b, Fs):
             if K == 0:
                 return x
             return orc.run(M, c, r, v, b, 0.0, tau, K, 0, x0=x.astype(np.float64), first_iter=k0,
-                           refresh_every=-1).x.astype(np.float32)
+                           ).x.astype(np.float32)
         obj = lambda x: orc.objective(M, c, r, v, b, 0.0, x.astype(np.float64))
         out[tau] = T.iters_to_eps(runner, obj, N, 1e-6, Fs)
     return out

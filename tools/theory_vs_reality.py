@@ -59,9 +59,12 @@ def theoretical_speedup(tau, omega, n):
 def iters_to_eps(runner, objective, n, eps, Fstar, max_iters=1 << 24):
     """Smallest K with F(x_K) - F* <= eps.  runner(x, k0, K) runs iterations
     k0..k0+K-1 in place on x (float array), objective(x) -> F.  Doubling finds a
-    bracket, bisection (re-running from the saved iterate) the exact K."""
+    bracket, bisection (re-running from the saved iterate) the exact K.  Returns
+    None if F stops moving above eps (the fp32 iterate's floor: x_i + delta_i
+    rounds back to x_i) or max_iters is reached."""
     x = np.zeros(n, dtype=np.float32)
-    if objective(x) - Fstar <= eps:
+    F = objective(x)
+    if F - Fstar <= eps:
         return 0
     done, step = 0, 1
     while True:
@@ -69,7 +72,11 @@ def iters_to_eps(runner, objective, n, eps, Fstar, max_iters=1 << 24):
             return None
         saved = x.copy()
         x = runner(x, done, step)
-        if objective(x) - Fstar <= eps:
+        Fnew = objective(x)
+        if step >= 1024 and Fnew >= F:
+            return None
+        F = Fnew
+        if F - Fstar <= eps:
             lo, hi = 0, step          # crossing in (done + lo, done + hi]
             while hi - lo > 1:
                 mid = (lo + hi) // 2
@@ -94,7 +101,7 @@ def gpu_counter(c, r, v, b, m, tau, seed=0):
     def runner(x, k0, K):
         xd = torch.from_numpy(x).to(dev)
         if K > 0:
-            prob.run(xd, tau, K, seed=seed, first_iter=k0, refresh_every=-1)
+            prob.run(xd, tau, K, seed=seed, first_iter=k0)  # default refresh R = ceil(2n/tau)
         return xd.cpu().numpy()
 
     def objective(x):
@@ -124,7 +131,7 @@ def main():
             prob.close()
             if tau == 1:
                 serial = K
-            row = {"omega": om, "tau": tau, "iters": K, "F_star": Fstar,
+            row = {"omega": om, "tau": tau, "iters": K, "F_star": Fstar, "eps": args.eps,
                    "empirical_speedup": (serial / K) if (serial and K) else None,
                    "theoretical_speedup": theoretical_speedup(tau, om, n)}
             rows.append(row)
