@@ -39,8 +39,9 @@ from paper_1212_0873_b200 import instances as I  # noqa: E402
 
 METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline) at 1 B200"
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
-VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed"}
-KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel"}
+VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", -1: "async"}
+KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
+                     -1: "pcdm_async_kernel"}
 # oracle iterations per reference step / cpu_baseline sample, per config
 REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4}
 CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24}
@@ -59,6 +60,8 @@ def parse():
     ap.add_argument("--sampling", default="nice", choices=["nice", "independent", "binomial"],
                     help="doubly uniform sampling (NEXT-1 rows); the headline is tau-nice")
     ap.add_argument("--p-b", type=float, default=0.5, help="binomial availability probability")
+    ap.add_argument("--async", dest="async_", action="store_true",
+                    help="asynchronous variant (NEXT-4, PAPER.md:1248): tau*iters updates per step, no barriers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -309,6 +312,10 @@ def bench_ours(args, world, rank, local):
 
     def one_step(xbuf):
         nonlocal step
+        if args.async_:
+            prob.run_async(xbuf, tau * iters, seed=run_seed, first_update=step * tau * iters, stream=stream)
+            step += 1
+            return
         prob.run(xbuf, tau, iters, seed=run_seed, first_iter=step * iters, variant=args.variant, sampling=gsamp,
                  stream=stream)
         step += 1
@@ -342,12 +349,12 @@ def bench_ours(args, world, rank, local):
     it_launches = sum(s["iter_launches"] for s in st_list)
     samp_ms = sum(s["sampler_ms"] for s in st_list)
     setup_ms = sum(s["setup_ms"] for s in st_list)
-    iters_per_launch = K * iters / max(it_launches, 1)
+    iters_per_launch = K * iters / max(it_launches, 1)  # async: tau updates count as one "iteration"
     alg_bytes_launch = BYTES_PER_NNZ * avg_c * size * iters_per_launch
     launch_ms = it_ms / max(it_launches, 1)
     achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
     peak, peak_src = hbm_peak()
-    traffic = ncu_traffic(cfg.name, iters_per_launch)
+    traffic = None if args.async_ else ncu_traffic(cfg.name, iters_per_launch)
     launches = sum(s["kernel_launches"] for s in st_list)
     nz = sum(s["nonzero_deltas"] for s in st_list)
 
@@ -403,6 +410,7 @@ def bench_ours(args, world, rank, local):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "omega": prob.omega, "beta": prob.beta(tau) if gsamp is None else prob.beta_sampling(gsamp),
+        "async": bool(args.async_),
         "F_final": F_final, "nonzero_step_frac": nz / (K * size * iters),
         "variant": VARIANT_NAMES.get(st0["variant"], "?"),
         "grid": {"ctas": st0["grid_ctas"], "threads": st0["threads_per_cta"], "lanes_per_column": st0["lanes_per_column"]},

@@ -173,6 +173,25 @@ PCDM_API pcdm_status pcdm_run_sampling(pcdm_problem *p, float *x, const pcdm_sam
                               uint64_t seed, int64_t first_iter, int64_t refresh_every, double beta_override,
                               int32_t variant, void *stream);
 
+/* pcdm_run_async -- the asynchronous variant the paper's experiments ran
+ * (SURVEY 8(f) NEXT-4), measured, not oracle-checked: every worker
+ * (a group of lanes; pcdm_last_run_stats().grid_ctas x threads / lanes of them)
+ * repeatedly picks a coordinate uniformly at random (update u = first_update ..
+ * first_update+updates-1 picks i from Philox counter (u lo, u hi, rho, tag 6)) and
+ * applies its soft-threshold step computed from whatever r holds at that moment;
+ * x_i and r are updated with atomics, so r = Ax - b holds whatever the
+ * interleaving (up to fp32 rounding) but the iterates are not deterministic.
+ *   tau_beta      beta = 1 + (omega-1)(tau_beta-1)/max(1,n-1); 0 = the number of
+ *                 concurrent workers (clamped to n)
+ *   beta_override > 0 replaces that beta
+ *   refresh_every r recomputed from scratch after every this many updates
+ *                 (0 = 2n, -1 = never)
+ * Needs the packed layout (max column length <= 62): EINVAL otherwise, or for
+ * updates < 0, non-finite x.  EDIVERGED as pcdm_run. */
+PCDM_API pcdm_status pcdm_run_async(pcdm_problem *p, float *x, int64_t updates, int64_t tau_beta,
+                           double beta_override, int64_t refresh_every, uint64_t first_update, uint64_t seed,
+                           void *stream);
+
 /* beta of thm:ESO-DU for `sampling` on this problem (fp64, host). */
 PCDM_API pcdm_status pcdm_beta_sampling(const pcdm_problem *p, const pcdm_sampling *sampling, double *beta);
 

@@ -105,6 +105,23 @@ struct PackedParams {
     int* flags;
     unsigned long long* nz_total;
 };
+// asynchronous variant (NEXT-4): no barriers, no sampler pass
+struct AsyncParams {
+    const int4* blocks;
+    float* x;
+    float* r;
+    int64_t n;
+    int64_t updates;      // coordinate updates of this launch (all groups together)
+    int64_t u0;           // global index of this launch's first update (resume)
+    uint64_t seed;
+    uint64_t reject_below;
+    float beta;
+    float lambda;
+    int* flags;
+    unsigned long long* nz_total;
+};
+int async_groups(int G, int sms, int* ctas);
+cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st, int64_t* launches);
 int packed_lanes(int64_t max_len);
 cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,

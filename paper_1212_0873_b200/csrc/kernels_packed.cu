@@ -144,6 +144,68 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
     }
 }
 
+// ---------------------------------------------------------------- asynchronous variant
+// What the paper's experiments ran: every worker repeatedly picks a
+// coordinate uniformly at random and updates it from whatever r currently holds, with
+// no barrier between workers.  Here a worker is a group of G lanes; update u (global
+// index, u = u0 .. u0 + updates - 1) is done by group u mod ngroups and picks
+// i = Lemire(Philox(counter (u lo, u hi, rho, tag 6), key seed)).  x_i and r are
+// updated with atomics (x_i += delta, r += delta a_i) so that r = Ax - b is kept
+// whatever the interleaving; the result is not deterministic (measured, not
+// oracle-checked; R20).
+template <int G>
+__global__ void __launch_bounds__(kThreads, 3) pcdm_async_kernel(AsyncParams A) {
+    const int t = threadIdx.x & (G - 1);
+    const unsigned gm = gmask_of<G>();
+    const int src = (threadIdx.x & 31) & ~(G - 1);
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int pair0 = 2 * (t - 1);
+    unsigned long long nz = 0;
+    for (int64_t q = gid; q < A.updates; q += ngroups) {
+        const uint64_t u = (uint64_t)(A.u0 + q);
+        int i = 0;
+        if (t == 0) {
+            long long v;
+            uint32_t rho = 0;
+            do {
+                u32x4 o = philox4x32_10(u32x4{(uint32_t)u, (uint32_t)(u >> 32), rho, 6u}, (uint32_t)A.seed,
+                                        (uint32_t)(A.seed >> 32));
+                const uint64_t w = ((uint64_t)o.y << 32) | (uint64_t)o.x;
+                v = (w * (uint64_t)A.n < A.reject_below) ? -1 : (long long)__umul64hi(w, (uint64_t)A.n);
+                ++rho;
+            } while (v < 0);
+            i = (int)v;
+        }
+        i = __shfl_sync(gm, i, src);
+        float xi = 0.0f;
+        if (t == 0) xi = ld_l2_f32(A.x + i);
+        const int4 c = ld_stream_v4(A.blocks + (int64_t)i * G + t);
+        const int len = __shfl_sync(gm, c.y, src);
+        float acc = 0.0f;
+        if (t > 0) {
+            const float ra = pair0 < len ? ld_l2_f32(A.r + c.x) : 0.0f;
+            const float rb = pair0 + 1 < len ? ld_l2_f32(A.r + c.z) : 0.0f;
+            acc = fmaf(__int_as_float(c.y), ra, __int_as_float(c.w) * rb);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gm, acc, o);
+        float d = 0.0f;
+        if (t == 0) {
+            const float xp = prox_l1(xi, acc, A.beta * __int_as_float(c.x), A.lambda);
+            d = xp - xi;
+            if (d != 0.0f) {
+                if (!isfinite(xp)) atomicOr(A.flags, FLAG_DIVERGED);
+                atomicAdd(A.x + i, d);
+                ++nz;
+            }
+        }
+        d = __shfl_sync(gm, d, src);
+        if (d != 0.0f && t > 0) scatter_chunk(A.r, c, pair0, len, d);
+    }
+    if (nz) atomicAdd(A.nz_total, nz);
+}
+
 // Pack the CSC into blocks: one thread per (column, chunk).
 __global__ void pack_kernel(int64_t n, int G, const long long* __restrict__ colptr, const int* __restrict__ rowidx,
                             const float* __restrict__ val, const float* __restrict__ L, int4* __restrict__ blocks) {
@@ -221,6 +283,34 @@ cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowi
     if (b > sms * 16) b = sms * 16;
     pack_kernel<<<(int)b, 256, 0, st>>>(n, G, (const long long*)colptr, rowidx, val, L, blocks);
     ++*launches;
+    return cudaGetLastError();
+}
+
+int async_groups(int G, int sms, int* ctas) {
+    const void* fn;
+    switch (G) {
+        case 2: fn = (const void*)pcdm_async_kernel<2>; break;
+        case 4: fn = (const void*)pcdm_async_kernel<4>; break;
+        case 8: fn = (const void*)pcdm_async_kernel<8>; break;
+        case 16: fn = (const void*)pcdm_async_kernel<16>; break;
+        default: fn = (const void*)pcdm_async_kernel<32>; break;
+    }
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    *ctas = per_sm * sms;
+    return *ctas * (kThreads / G);
+}
+
+cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st, int64_t* launches) {
+    ++*launches;
+    switch (G) {
+        case 2: pcdm_async_kernel<2><<<ctas, kThreads, 0, st>>>(A); break;
+        case 4: pcdm_async_kernel<4><<<ctas, kThreads, 0, st>>>(A); break;
+        case 8: pcdm_async_kernel<8><<<ctas, kThreads, 0, st>>>(A); break;
+        case 16: pcdm_async_kernel<16><<<ctas, kThreads, 0, st>>>(A); break;
+        default: pcdm_async_kernel<32><<<ctas, kThreads, 0, st>>>(A); break;
+    }
     return cudaGetLastError();
 }
 

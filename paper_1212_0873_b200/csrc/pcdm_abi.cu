@@ -684,6 +684,94 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
 
 extern "C" {
 
+pcdm_status pcdm_run_async(pcdm_problem* p, float* x, int64_t updates, int64_t tau_beta, double beta_override,
+                           int64_t refresh_every, uint64_t first_update, uint64_t seed, void* stream) {
+    if (!p || !x) return fail(PCDM_EINVAL, "NULL argument");
+    if (updates < 0 || tau_beta < 0) return fail(PCDM_EINVAL, "updates and tau_beta must be >= 0");
+    if (!p->packed_G)
+        return fail(PCDM_EINVAL, "asynchronous variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
+    if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
+    CK(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    pcdm_run_stats stats{};
+    int64_t launches = 0;
+    RunTimer tm{p, st};
+    int t0;
+    CK(tm.begin(&t0), "event");
+    const bool x_dev = is_device_ptr(x);
+    float* xd = x;
+    if (!x_dev) {
+        if (!p->xbuf) CK(cudaMalloc((void**)&p->xbuf, sizeof(float) * p->n), "alloc x buffer");
+        CK(cudaMemcpyAsync(p->xbuf, x, sizeof(float) * p->n, cudaMemcpyHostToDevice, st), "copy x in");
+        xd = p->xbuf;
+    }
+    CK(cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st), "memset scalars");
+    pcdm_status s = residual_from(p, xd, st, &launches);
+    if (s != PCDM_OK) return s;
+    CK(tm.end(T_SETUP, t0), "event");
+    Scalars hs{};
+    if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
+    if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
+
+    int ctas = 0;
+    const int64_t workers = async_groups(p->packed_G, p->sms, &ctas);
+    const int64_t tb = std::min<int64_t>(tau_beta > 0 ? tau_beta : workers, p->n);
+    double beta_d = 1.0 + (double)(p->omega - 1) * (double)(tb - 1) / (double)std::max<int64_t>(1, p->n - 1);
+    if (beta_override > 0.0) beta_d = beta_override;
+    const int64_t R = refresh_every < 0 ? 0 : (refresh_every > 0 ? refresh_every : 2 * p->n);
+    AsyncParams A{};
+    A.blocks = p->blocks;
+    A.x = xd;
+    A.r = p->r;
+    A.n = p->n;
+    A.seed = seed;
+    A.reject_below = (uint64_t)(0 - (uint64_t)p->n) % (uint64_t)p->n;
+    A.beta = (float)beta_d;
+    A.lambda = (float)p->lambda;
+    A.flags = &p->sc->flags;
+    A.nz_total = &p->sc->nz_total;
+    for (int64_t done = 0; done < updates;) {
+        const int64_t c = R > 0 ? std::min(R, updates - done) : updates - done;
+        A.updates = c;
+        A.u0 = (int64_t)(first_update + (uint64_t)done);
+        int ti;
+        CK(tm.begin(&ti), "event");
+        CK(launch_async(p->packed_G, ctas, A, st, &launches), "async kernel");
+        CK(tm.end(T_ITER, ti), "event");
+        ++stats.iter_launches;
+        done += c;
+        if (R > 0 && done < updates) {
+            int tr;
+            CK(tm.begin(&tr), "event");
+            if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) return s;
+            CK(tm.end(T_SETUP, tr), "event");
+            ++stats.refreshes;
+        }
+    }
+    p->r_cur = p->r;
+    int tx;
+    CK(tm.begin(&tx), "event");
+    if (!x_dev) CK(cudaMemcpyAsync(x, p->xbuf, sizeof(float) * p->n, cudaMemcpyDeviceToHost, st), "copy x out");
+    CK(tm.end(T_SETUP, tx), "event");
+    if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
+    stats.iters = updates;
+    stats.nonzero_deltas = (int64_t)hs.nz_total;
+    stats.kernel_launches = launches;
+    stats.variant = -1;
+    stats.grid_ctas = ctas;
+    stats.threads_per_cta = 512;
+    stats.lanes_per_column = p->packed_G;
+    stats.chunk_iters = R > 0 ? R : updates;
+    double tms[3];
+    tm.sum(tms);
+    stats.iter_kernel_ms = tms[T_ITER];
+    stats.sampler_ms = 0.0;
+    stats.setup_ms = tms[T_SETUP];
+    p->stats = stats;
+    if (hs.flags & FLAG_DIVERGED) return fail(PCDM_EDIVERGED, "non-finite step (diverged)");
+    return PCDM_OK;
+}
+
 pcdm_status pcdm_objective(pcdm_problem* p, const float* x, double* F, void* stream) {
     if (!p || !x || !F) return fail(PCDM_EINVAL, "NULL argument");
     CK(cudaSetDevice(p->device), "cudaSetDevice");

@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EDIVERGED", 5
 EXPORTS = ["pcdm_create", "pcdm_destroy", "pcdm_last_error", "pcdm_omega", "pcdm_beta", "pcdm_run",
            "pcdm_run_ex", "pcdm_objective", "pcdm_last_run_stats", "pcdm_sample", "pcdm_col_norms",
            "pcdm_row_counts", "pcdm_residual", "pcdm_philox", "pcdm_philox_check_curand",
-           "pcdm_run_sampling", "pcdm_beta_sampling", "pcdm_sample_sampling"]
+           "pcdm_run_sampling", "pcdm_beta_sampling", "pcdm_sample_sampling", "pcdm_run_async"]
 SAMPLING_KINDS = {"nice": 0, "independent": 1, "binomial": 2, "du": 3}
 
 
@@ -98,6 +98,7 @@ def load():
         "pcdm_philox": ([i64, P, P, P, P], st),
         "pcdm_philox_check_curand": ([i64, u64, ctypes.POINTER(i64), P], st),
         "pcdm_run_sampling": ([P, P, ctypes.POINTER(_CSampling), i64, u64, i64, i64, f64, i32, P], st),
+        "pcdm_run_async": ([P, P, i64, i64, f64, i64, u64, u64, P], st),
         "pcdm_beta_sampling": ([P, ctypes.POINTER(_CSampling), ctypes.POINTER(f64)], st),
         "pcdm_sample_sampling": ([i64, ctypes.POINTER(_CSampling), u64, i64, i64, P, P], st),
     }
@@ -191,6 +192,12 @@ def pcdm_run_sampling(h, x, sampling: Sampling, iters, seed, first_iter=0, refre
     cs = sampling.c()
     _check(load().pcdm_run_sampling(h, _ptr(x, "f32"), ctypes.byref(cs), int(iters), int(seed), int(first_iter),
                                     int(refresh_every), float(beta_override), v, _stream(stream)))
+
+
+def pcdm_run_async(h, x, updates, tau_beta=0, beta_override=0.0, refresh_every=0, first_update=0, seed=0,
+                   stream=None):
+    _check(load().pcdm_run_async(h, _ptr(x, "f32"), int(updates), int(tau_beta), float(beta_override),
+                                 int(refresh_every), int(first_update), int(seed), _stream(stream)))
 
 
 def pcdm_beta_sampling(h, sampling: Sampling) -> float:
@@ -296,6 +303,12 @@ class Problem:
         else:
             pcdm_run_sampling(self.handle, x, sampling, iters, seed, first_iter, refresh_every, beta_override,
                               variant, stream)
+        return x
+
+    def run_async(self, x, updates, tau_beta=0, beta_override=0.0, refresh_every=0, first_update=0, seed=0,
+                  stream=None):
+        """Asynchronous variant (NEXT-4): `updates` coordinate updates, no barriers."""
+        pcdm_run_async(self.handle, x, updates, tau_beta, beta_override, refresh_every, first_update, seed, stream)
         return x
 
     def beta_sampling(self, sampling: Sampling):
