@@ -76,6 +76,19 @@ def _load():
     lib.or_run_kind.argtypes = [i64, i64, P, P, P, P, f64, P, f64, P, i32, i64, f64, P, i64, u64, i64, i64,
                                 P, P, ctypes.POINTER(ctypes.c_double)]
     lib.or_run_kind.restype = i32
+    lib.or_margins.argtypes = [i64, i64, P, P, P, P, P, P]
+    lib.or_margins.restype = None
+    lib.or_logistic_objective.argtypes = [i64, i64, P, P, P, P, f64, P]
+    lib.or_logistic_objective.restype = f64
+    lib.or_logistic_grad_i.argtypes = [P, P, P, P, P, i64]
+    lib.or_logistic_grad_i.restype = f64
+    lib.or_logistic_L.argtypes = [i64, P, P, P]
+    lib.or_logistic_L.restype = None
+    lib.or_logistic_step.argtypes = [f64, f64, f64, f64]
+    lib.or_logistic_step.restype = f64
+    lib.or_logistic_run.argtypes = [i64, i64, P, P, P, P, f64, P, f64, P, i32, i64, f64, P, i64, u64, i64, i64,
+                                    P, ctypes.POINTER(ctypes.c_double)]
+    lib.or_logistic_run.restype = i32
     _lib = lib
     return lib
 
@@ -265,3 +278,67 @@ def run(m, colptr, rowidx, val, b, lam, tau, iters, seed, x0=None, first_iter=0,
     if rc == 1:
         raise FloatingPointError("oracle: non-finite delta (diverged)")
     return RunResult(x, r, slots.reshape(iters, tau) if keep_slots else None, secs.value, om, bt, Lv)
+
+
+# ---------------------------------------------------------------- L2-regularised logistic regression (NEXT-3)
+def margins(m, colptr, rowidx, val, y, x) -> np.ndarray:
+    """s_j = y_j (Ax)_j in fp64."""
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s = np.empty(m, dtype=np.float64)
+    _load().or_margins(m, colptr.size - 1, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(y), _ptr(x), _ptr(s))
+    return s
+
+
+def logistic_objective(m, colptr, rowidx, val, y, lam, x) -> float:
+    """F(x) = sum_j log(1 + exp(-y_j A_j^T x)) + lambda ||x||^2 (Sec. 8.4)."""
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return float(_load().or_logistic_objective(m, colptr.size - 1, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(y),
+                                               lam, _ptr(x)))
+
+
+def logistic_grad_i(colptr, rowidx, val, y, s, i) -> float:
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    return float(_load().or_logistic_grad_i(_ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(y), _ptr(s), i))
+
+
+def logistic_L(colptr, val) -> np.ndarray:
+    colptr = np.ascontiguousarray(colptr, dtype=np.int64)
+    val = np.ascontiguousarray(val, dtype=np.float32)
+    n = colptr.size - 1
+    L = np.empty(n, dtype=np.float64)
+    _load().or_logistic_L(n, _ptr(colptr), _ptr(val), _ptr(L))
+    return L
+
+
+def logistic_step(x, g, s, lam) -> float:
+    return float(_load().or_logistic_step(x, g, s, lam))
+
+
+def logistic_run(m, colptr, rowidx, val, y, lam, tau, iters, seed, x0=None, first_iter=0, refresh_every=0,
+                 beta_override=None, sampling: Sampling = None):
+    """Synchronous PCDM1 on the L2-regularised logistic problem (O5-O8 with margins)."""
+    colptr, rowidx, val = _csc(colptr, rowidx, val)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    n = colptr.size - 1
+    om = omega(m, rowidx)
+    L = logistic_L(colptr, val)
+    S = sampling if sampling is not None else Sampling("nice", tau)
+    bt = float(beta_override) if beta_override is not None else (
+        beta(om, S.tau, n) if S.kind == "nice" else beta_sampling(om, n, S))
+    x = np.zeros(n, dtype=np.float64) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    s = np.empty(m, dtype=np.float64)
+    secs = ctypes.c_double(0.0)
+    rc = _load().or_logistic_run(m, n, _ptr(colptr), _ptr(rowidx), _ptr(val), _ptr(y), lam, _ptr(L), bt, _ptr(x),
+                                 KINDS[S.kind], S.tau, S.p_b, S._q(), iters, seed, first_iter, refresh_every,
+                                 _ptr(s), ctypes.byref(secs))
+    if rc < 0:
+        raise ValueError("or_logistic_run failed (rc=%d)" % rc)
+    if rc == 1:
+        raise FloatingPointError("oracle: non-finite step")
+    return RunResult(x, s, None, secs.value, om, bt, L)

@@ -457,3 +457,123 @@ int or_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx,
     return or_run_kind(m, n, colptr, rowidx, val, b, lambda, L, beta, x, OR_NICE, tau, 0.0, NULL, iters,
                        seed, first_iter, refresh_every, r_out, slots_out, loop_seconds);
 }
+
+/* ------------------------------------------------------------------------ */
+/* L2-regularised logistic regression (Sec. 8.4,         */
+/* PAPER.md:1381-1392; logistic loss of tbl:ML3 PAPER.md:68):                */
+/*   F(x) = sum_j log(1 + exp(-y_j A_j^T x)) + lambda ||x||_2^2,             */
+/* y_j in {+1,-1}.  Unit blocks, Omega_i(t) = lambda t^2 (eq:Psi_block_def   */
+/* PAPER.md:155-159).  Reading R21: block Lipschitz constants    */
+/* L_i = 1/4 ||a_i||^2 (the logistic loss has curvature <= 1/4), the update  */
+/* minimises <grad_i f, t> + (beta L_i / 2) t^2 + lambda (x_i + t)^2 exactly: */
+/*   t = -(grad_i f + 2 lambda x_i) / (beta L_i + 2 lambda),                 */
+/* with grad_i f = -sum_j y_j a_ji sigma(-s_j), s_j = y_j A_j^T x (margins), */
+/* sigma(z) = 1 / (1 + exp(-z)).                                            */
+/* ------------------------------------------------------------------------ */
+static double or_sigma(double z)
+{
+    return z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+}
+
+/* log(1 + exp(-s)) without overflow */
+static double or_logloss(double s)
+{
+    return s >= 0.0 ? log1p(exp(-s)) : -s + log1p(exp(s));
+}
+
+/* margins s_j = y_j (A x)_j from scratch, in double */
+void or_margins(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx, const float *val,
+                const float *y, const double *x, double *s)
+{
+    for (int64_t j = 0; j < m; ++j) s[j] = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (x[i] == 0.0) continue;
+        for (int64_t p = colptr[i]; p < colptr[i + 1]; ++p)
+            s[rowidx[p]] += (double)val[p] * x[i];
+    }
+    for (int64_t j = 0; j < m; ++j) s[j] *= (double)y[j];
+}
+
+double or_logistic_objective(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx, const float *val,
+                             const float *y, double lambda, const double *x)
+{
+    double *s = (double *)malloc(sizeof(double) * (size_t)m);
+    or_margins(m, n, colptr, rowidx, val, y, x, s);
+    double f = 0.0;
+    for (int64_t j = 0; j < m; ++j) f += or_logloss(s[j]);
+    double q = 0.0;
+    for (int64_t i = 0; i < n; ++i) q += x[i] * x[i];
+    free(s);
+    return f + lambda * q;
+}
+
+/* grad_i f at the margins s (for tests) */
+double or_logistic_grad_i(const int64_t *colptr, const int32_t *rowidx, const float *val, const float *y,
+                          const double *s, int64_t i)
+{
+    double g = 0.0;
+    for (int64_t p = colptr[i]; p < colptr[i + 1]; ++p)
+        g -= (double)y[rowidx[p]] * (double)val[p] * or_sigma(-s[rowidx[p]]);
+    return g;
+}
+
+/* L_i = 1/4 ||a_i||^2 */
+void or_logistic_L(int64_t n, const int64_t *colptr, const float *val, double *L)
+{
+    or_col_norms(n, colptr, val, L);
+    for (int64_t i = 0; i < n; ++i) L[i] *= 0.25;
+}
+
+/* block update: x+ = x + t, t = -(g + 2 lambda x) / (s + 2 lambda), s = beta L_i.
+ * s + 2 lambda = 0 (empty column, lambda = 0): x unchanged (reading R21). */
+double or_logistic_step(double x, double g, double s, double lambda)
+{
+    double d = s + 2.0 * lambda;
+    if (d == 0.0) return x;
+    return x - (g + 2.0 * lambda * x) / d;
+}
+
+/* Synchronous PCDM1 for the logistic problem: the same O5-O8 structure as
+ * or_run_kind with the margins s in place of r (O4: s = y .* (Ax); O6 reads
+ * sigma(-s) of the snapshot; O7 adds y_j a_ji delta; O8 recomputes s). */
+int or_logistic_run(int64_t m, int64_t n, const int64_t *colptr, const int32_t *rowidx, const float *val,
+                    const float *y, double lambda, const double *L, double beta, double *x, int kind, int64_t tau,
+                    double p_b, const double *q, int64_t iters, uint64_t seed, int64_t first_iter,
+                    int64_t refresh_every, double *s_out, double *loop_seconds)
+{
+    if (m < 1 || n < 1 || tau < 1 || tau > n || iters < 0 || first_iter < 0) return -1;
+    double *s = (double *)malloc(sizeof(double) * (size_t)m);
+    int32_t *S = (int32_t *)malloc(sizeof(int32_t) * (size_t)tau);
+    double *xplus = (double *)malloc(sizeof(double) * (size_t)tau);
+    if (!s || !S || !xplus) return -1;
+    int64_t R = or_refresh_period(n, tau, refresh_every);
+    int rc = 0;
+    or_margins(m, n, colptr, rowidx, val, y, x, s);
+    double t0 = now_seconds();
+    for (int64_t it = 0; it < iters && rc == 0; ++it) {
+        int64_t k = first_iter + it;
+        if (or_sample_kind(kind, seed, k, tau, n, p_b, q, S) != 0) { rc = -2; break; }
+        for (int64_t j = 0; j < tau; ++j) {
+            int64_t i = S[j];
+            if (i < 0) continue;
+            double g = or_logistic_grad_i(colptr, rowidx, val, y, s, i);
+            xplus[j] = or_logistic_step(x[i], g, beta * L[i], lambda);
+            if (!isfinite(xplus[j])) rc = 1;
+        }
+        for (int64_t j = 0; j < tau; ++j) {
+            int64_t i = S[j];
+            if (i < 0) continue;
+            double delta = xplus[j] - x[i];
+            x[i] = xplus[j];
+            for (int64_t p = colptr[i]; p < colptr[i + 1]; ++p)
+                s[rowidx[p]] += (double)y[rowidx[p]] * (double)val[p] * delta;
+        }
+        if (R > 0 && (it + 1) % R == 0)
+            or_margins(m, n, colptr, rowidx, val, y, x, s);
+    }
+    double t1 = now_seconds();
+    if (loop_seconds) *loop_seconds = t1 - t0;
+    if (s_out) memcpy(s_out, s, sizeof(double) * (size_t)m);
+    free(s); free(S); free(xplus);
+    return rc;
+}

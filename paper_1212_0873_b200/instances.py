@@ -252,3 +252,42 @@ def equal_row_random_matrix(m: int, n: int, omega: int, seed: int = 0):
     colptr = torch.zeros(n + 1, dtype=torch.int64)
     colptr[1:] = torch.cumsum(counts, 0)
     return colptr, row_sorted.to(torch.int32), torch.ones(m * omega, dtype=torch.float32)
+
+
+# L2-regularised logistic regression (Sec. 8.4): KDDB is not
+# available, so a synthetic instance with its shape stands in for it (DESIGN.md
+# "Input recipe"): n features (columns), m examples (rows), c nonzeros per feature
+# at uniform distinct examples, N(0,1) values, labels y = sign(A w* + 0.1 eps) with
+# a 1 %-dense planted w*, lambda = 1 (the paper's value).
+LOGISTIC_CONFIGS = {
+    "logistic_small": InstanceConfig("logistic_small", 20_000, 30_000, 19, 300, tau=1024, iters=2000),
+    "kddb_like": InstanceConfig("kddb_like", 19_264_097, 29_890_095, 19, 298_900, tau=1 << 16, iters=500),
+}
+
+
+def generate_logistic(cfg, seed: int = 0, device="cpu", lam: float = 1.0, chunk_cols: int = 1 << 23):
+    """(colptr, rowidx, val, y, lam) for a logistic config (name or InstanceConfig)."""
+    if isinstance(cfg, str):
+        cfg = LOGISTIC_CONFIGS[cfg]
+    device = torch.device(device)
+    m, n, c = cfg.m, cfg.n, cfg.nnz_per_col
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    rowidx = torch.empty(n * c, dtype=torch.int32, device=device)
+    val = torch.empty(n * c, dtype=torch.float32, device=device)
+    for c0 in range(0, n, chunk_cols):
+        k = min(chunk_cols, n - c0)
+        rows = _draw_rows(k, c, m, gen, device, None)
+        rowidx[c0 * c:(c0 + k) * c] = rows.view(-1).to(torch.int32)
+        del rows
+        val[c0 * c:(c0 + k) * c] = torch.randn(k * c, generator=gen, device=device, dtype=torch.float32)
+    colptr = torch.arange(0, n + 1, dtype=torch.int64, device=device) * c
+    s = min(cfg.s_star, n)
+    widx = torch.randperm(n, generator=gen, device=device)[:s]
+    wval = torch.randn(s, generator=gen, device=device, dtype=torch.float64)
+    z = torch.zeros(m, dtype=torch.float64, device=device)
+    pos = (widx.view(-1, 1) * c + torch.arange(c, device=device).view(1, -1)).view(-1)
+    z.index_add_(0, rowidx[pos].to(torch.int64), val[pos].to(torch.float64) * wval.repeat_interleave(c))
+    z += 0.1 * torch.randn(m, generator=gen, device=device, dtype=torch.float64)
+    y = torch.where(z >= 0, 1.0, -1.0).to(torch.float32)
+    return colptr, rowidx, val, y, float(lam)
