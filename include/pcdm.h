@@ -131,6 +131,23 @@ PCDM_API pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_
                         const int32_t *rowidx, const float *val, const float *b, double lambda,
                         void *stream, pcdm_problem **out);
 
+/* pcdm_create_logistic -- the L2-regularised logistic regression problem of Sec. 8.4
+ * (logistic loss of tbl:ML3 PAPER.md:68):
+ *
+ *     minimise  F(x) = sum_j log(1 + exp(-y_j A_j^T x)) + lambda ||x||_2^2,
+ *
+ * rows of A = examples, columns = features, labels y float32[m] in {+1, -1}.
+ * Same CSC arguments, ownership and errors as pcdm_create (EINVAL also for a label
+ * other than +-1).  The library stores A~ = diag(y) A; the maintained vector r is the
+ * margin s = A~ x; L_i = ||a_i||^2 / 4; omega as for LASSO; the block step minimises
+ * grad_i f t + (beta L_i / 2) t^2 + lambda (x_i + t)^2 exactly (R21).
+ * pcdm_run / pcdm_run_ex / pcdm_run_sampling / pcdm_objective / pcdm_residual
+ * (returns s) / pcdm_col_norms (returns L) work on the handle; pcdm_run_async does
+ * not (EINVAL). */
+PCDM_API pcdm_status pcdm_create_logistic(int64_t m, int64_t n, int64_t nnz, const int64_t *colptr,
+                                 const int32_t *rowidx, const float *val, const float *y, double lambda,
+                                 void *stream, pcdm_problem **out);
+
 /* Frees every device buffer of the handle (NULL is a no-op). */
 PCDM_API void pcdm_destroy(pcdm_problem *p);
 

@@ -160,4 +160,26 @@ __device__ __forceinline__ float prox_l1(float x, float g, float s, float lam) {
     return u > 0.0f ? mag : -mag;
 }
 
+// ---------------------------------------------------------------- losses
+// LASSO (square loss): the gathered vector is r = Ax - b, grad_i f = sum_j a_ji r_j,
+// block step = soft-threshold (eq:h(x) block form).
+// L2-regularised logistic (Sec. 8.4; R21): the library
+// stores A~ = diag(y) A, the gathered vector is the margin s = A~ x,
+// grad_i f = -sum_j a~_ji sigma(-s_j) = sum_j a~_ji w(s_j), w(s) = -1/(1+e^s), and the
+// step minimises g t + (beta L_i/2) t^2 + lambda (x+t)^2 exactly.
+template <bool LOGISTIC>
+__device__ __forceinline__ float grad_weight(float v) {
+    if (LOGISTIC) return -1.0f / (1.0f + __expf(v));
+    return v;
+}
+
+template <bool LOGISTIC>
+__device__ __forceinline__ float block_step(float x, float g, float s, float lam) {
+    if (LOGISTIC) {
+        const float d = s + 2.0f * lam;
+        return d == 0.0f ? x : x - (g + 2.0f * lam * x) / d;
+    }
+    return prox_l1(x, g, s, lam);
+}
+
 }  // namespace pcdm

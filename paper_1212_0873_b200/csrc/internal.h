@@ -26,6 +26,14 @@ cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t 
 cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
                                   cudaStream_t st, int sms, int64_t* launches);
 
+// L2-regularised logistic problem (NEXT-3): label check (+-1, flags FLAG_NONFINITE_B
+// otherwise) and A~ = diag(y) A in place; L scaling; objective sums
+cudaError_t launch_logistic_setup(int64_t m, int64_t nnz, const int* rowidx, const float* y, float* val, int* flags,
+                                  cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_scale(int64_t n, float a, float* v, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_objective_logistic(int64_t m, int64_t n, const double* s64, const float* x, double* out,
+                                      cudaStream_t st, int sms, int64_t* launches);
+
 // ---- samplers (kernels_sampler.cu)
 // Doubly uniform samplings of PAPER.md:418-456 (pcdm_sampling_kind); the slot
 // arrays hold tau entries per iteration, -1 for an idle processor.
@@ -78,6 +86,7 @@ struct IterParams {
     int* flags;
     unsigned long long* nz_total;  // accumulates #delta != 0
     int64_t m, n;
+    int logistic;         // 1: L2-regularised logistic loss (margins in r)
 };
 
 struct IterLaunch {
@@ -104,6 +113,7 @@ struct PackedParams {
     unsigned* barrier;
     int* flags;
     unsigned long long* nz_total;
+    int logistic;         // 1: L2-regularised logistic loss (margins in r0/r1)
 };
 // asynchronous variant (NEXT-4): no barriers, no sampler pass
 struct AsyncParams {
@@ -126,12 +136,13 @@ int packed_lanes(int64_t max_len);
 cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
                         int4* blocks, cudaStream_t st, int sms, int64_t* launches);
-int packed_ctas(int G, bool one_barrier, int sms);
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false);
 cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
                           int64_t* launches);
 
 // Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
-IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device);
+IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,
+                     bool logistic = false);
 cudaError_t launch_iter(const IterLaunch& L, const IterParams& P, cudaStream_t st, int64_t* launches);
 
 }  // namespace pcdm_internal

@@ -48,7 +48,7 @@ __device__ __forceinline__ unsigned group_mask() {
 }
 
 // G lanes per sampled column, U entries per lane in flight.
-template <int G, int U, bool SINGLE>
+template <int G, int U, bool SINGLE, bool LOGISTIC>
 __global__ void __launch_bounds__(kGridThreads) pcdm_iter_kernel(IterParams P) {
     const int lane_g = threadIdx.x & (G - 1);
     const unsigned gmask = group_mask<G>();
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kGridThreads) pcdm_iter_kernel(IterParams P) {
                 }
                 float gv[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) gv[u] = rr[u] >= 0 ? ld_l2_f32(P.r + rr[u]) : 0.0f;
+                for (int u = 0; u < U; ++u) gv[u] = rr[u] >= 0 ? grad_weight<LOGISTIC>(ld_l2_f32(P.r + rr[u])) : 0.0f;
 #pragma unroll
                 for (int u = 0; u < U; ++u) acc = fmaf(vv[u], gv[u], acc);
             }
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kGridThreads) pcdm_iter_kernel(IterParams P) {
             if (lane_g == 0) {
                 const float Li = ld_stream_f32(P.L + i);
                 const float xi = ld_l2_f32(P.x + i);
-                const float xp = prox_l1(xi, acc, beta * Li, lam);
+                const float xp = block_step<LOGISTIC>(xi, acc, beta * Li, lam);
                 const float d = xp - xi;
                 if (d != 0.0f) {
                     if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kGridThreads) pcdm_iter_kernel(IterParams P) {
 // int32 offsets, (row, val), L, x, r; lists of nonzero steps too.
 constexpr int kSmemThreads = 1024;
 
-template <int G>
+template <int G, bool LOGISTIC>
 __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = (int)P.m, n = (int)P.n;
@@ -169,12 +169,12 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
             float acc = 0.0f;
             for (int base = s; base < e; base += G) {
                 const int q = base + lane_g;
-                if (q < e) acc = fmaf(s_val[q], s_r[s_row[q]], acc);
+                if (q < e) acc = fmaf(s_val[q], grad_weight<LOGISTIC>(s_r[s_row[q]]), acc);
             }
             acc = group_sum<G>(acc, gmask);
             if (lane_g == 0) {
                 const float xi = s_x[i];
-                const float xp = prox_l1(xi, acc, beta * s_L[i], lam);
+                const float xp = block_step<LOGISTIC>(xi, acc, beta * s_L[i], lam);
                 const float d = xp - xi;
                 if (d != 0.0f) {
                     if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
@@ -212,36 +212,57 @@ int pow2_clamp(int64_t v, int lo, int hi) {
     return g < lo ? lo : g;
 }
 
-template <int G, int U, bool SINGLE>
+template <int G, int U, bool SINGLE, bool LOG>
 cudaError_t launch_one(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
     if (SINGLE) {
-        pcdm_iter_kernel<G, U, true><<<1, L.threads, 0, st>>>(P);
+        pcdm_iter_kernel<G, U, true, LOG><<<1, L.threads, 0, st>>>(P);
         return cudaGetLastError();
     }
     void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel((const void*)pcdm_iter_kernel<G, U, false>, dim3(L.ctas), dim3(L.threads),
-                                       args, 0, st);
+    return cudaLaunchCooperativeKernel((const void*)pcdm_iter_kernel<G, U, false, LOG>, dim3(L.ctas),
+                                       dim3(L.threads), args, 0, st);
 }
 
-template <int U, bool SINGLE>
+template <int U, bool SINGLE, bool LOG>
 cudaError_t launch_lanes(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
     switch (L.lanes) {
-        case 1: return launch_one<1, U, SINGLE>(L, P, st);
-        case 2: return launch_one<2, U, SINGLE>(L, P, st);
-        case 4: return launch_one<4, U, SINGLE>(L, P, st);
-        case 8: return launch_one<8, U, SINGLE>(L, P, st);
-        case 16: return launch_one<16, U, SINGLE>(L, P, st);
-        default: return launch_one<32, U, SINGLE>(L, P, st);
+        case 1: return launch_one<1, U, SINGLE, LOG>(L, P, st);
+        case 2: return launch_one<2, U, SINGLE, LOG>(L, P, st);
+        case 4: return launch_one<4, U, SINGLE, LOG>(L, P, st);
+        case 8: return launch_one<8, U, SINGLE, LOG>(L, P, st);
+        case 16: return launch_one<16, U, SINGLE, LOG>(L, P, st);
+        default: return launch_one<32, U, SINGLE, LOG>(L, P, st);
     }
 }
 
-template <int G>
+template <int G, bool LOG>
 cudaError_t launch_smem(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(pcdm_smem_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(pcdm_smem_kernel<G, LOG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)L.smem);
     if (e != cudaSuccess) return e;
-    pcdm_smem_kernel<G><<<1, L.threads, L.smem, st>>>(P);
+    pcdm_smem_kernel<G, LOG><<<1, L.threads, L.smem, st>>>(P);
     return cudaGetLastError();
+}
+
+}  // namespace
+
+namespace {
+
+template <bool LOG>
+cudaError_t launch_iter_loss(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
+    constexpr int kU = 8;
+    if (L.variant == 2) {
+        switch (L.lanes) {
+            case 1: return launch_smem<1, LOG>(L, P, st);
+            case 2: return launch_smem<2, LOG>(L, P, st);
+            case 4: return launch_smem<4, LOG>(L, P, st);
+            case 8: return launch_smem<8, LOG>(L, P, st);
+            case 16: return launch_smem<16, LOG>(L, P, st);
+            default: return launch_smem<32, LOG>(L, P, st);
+        }
+    }
+    if (L.variant == 3) return launch_lanes<kU, true, LOG>(L, P, st);
+    return launch_lanes<kU, false, LOG>(L, P, st);
 }
 
 }  // namespace
@@ -251,7 +272,8 @@ namespace pcdm_internal {
 constexpr int kUnroll = 8;
 constexpr size_t kSmemLimit = 200 * 1024;
 
-IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device) {
+IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,
+                     bool logistic) {
     IterLaunch L{};
     const int64_t avg = (nnz + n - 1) / n;
     const size_t sm = smem_bytes(m, n, nnz, tau);
@@ -274,12 +296,12 @@ IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau
     int per_sm = 1;
     const void* fn;
     switch (L.lanes) {
-        case 1: fn = (const void*)pcdm_iter_kernel<1, kUnroll, false>; break;
-        case 2: fn = (const void*)pcdm_iter_kernel<2, kUnroll, false>; break;
-        case 4: fn = (const void*)pcdm_iter_kernel<4, kUnroll, false>; break;
-        case 8: fn = (const void*)pcdm_iter_kernel<8, kUnroll, false>; break;
-        case 16: fn = (const void*)pcdm_iter_kernel<16, kUnroll, false>; break;
-        default: fn = (const void*)pcdm_iter_kernel<32, kUnroll, false>; break;
+        case 1: fn = logistic ? (const void*)pcdm_iter_kernel<1, kUnroll, false, true> : (const void*)pcdm_iter_kernel<1, kUnroll, false, false>; break;
+        case 2: fn = logistic ? (const void*)pcdm_iter_kernel<2, kUnroll, false, true> : (const void*)pcdm_iter_kernel<2, kUnroll, false, false>; break;
+        case 4: fn = logistic ? (const void*)pcdm_iter_kernel<4, kUnroll, false, true> : (const void*)pcdm_iter_kernel<4, kUnroll, false, false>; break;
+        case 8: fn = logistic ? (const void*)pcdm_iter_kernel<8, kUnroll, false, true> : (const void*)pcdm_iter_kernel<8, kUnroll, false, false>; break;
+        case 16: fn = logistic ? (const void*)pcdm_iter_kernel<16, kUnroll, false, true> : (const void*)pcdm_iter_kernel<16, kUnroll, false, false>; break;
+        default: fn = logistic ? (const void*)pcdm_iter_kernel<32, kUnroll, false, true> : (const void*)pcdm_iter_kernel<32, kUnroll, false, false>; break;
     }
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridThreads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 1;
@@ -290,18 +312,7 @@ IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau
 
 cudaError_t launch_iter(const IterLaunch& L, const IterParams& P, cudaStream_t st, int64_t* launches) {
     ++*launches;
-    if (L.variant == 2) {
-        switch (L.lanes) {
-            case 1: return launch_smem<1>(L, P, st);
-            case 2: return launch_smem<2>(L, P, st);
-            case 4: return launch_smem<4>(L, P, st);
-            case 8: return launch_smem<8>(L, P, st);
-            case 16: return launch_smem<16>(L, P, st);
-            default: return launch_smem<32>(L, P, st);
-        }
-    }
-    if (L.variant == 3) return launch_lanes<kUnroll, true>(L, P, st);
-    return launch_lanes<kUnroll, false>(L, P, st);
+    return P.logistic ? launch_iter_loss<true>(L, P, st) : launch_iter_loss<false>(L, P, st);
 }
 
 }  // namespace pcdm_internal

@@ -62,7 +62,7 @@ __device__ __forceinline__ void scatter_chunk(float* r, const int4 c, int pair0,
     if (pair0 + 1 < len) red_add_f32(r + c.z, __int_as_float(c.w) * d);
 }
 
-template <int G, bool ONE_BARRIER>
+template <int G, bool ONE_BARRIER, bool LOGISTIC>
 __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P) {
     const int t = threadIdx.x & (G - 1);  // lane within the column group
     const unsigned gm = gmask_of<G>();
@@ -91,15 +91,15 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
             const int len = __shfl_sync(gm, c.y, src);
             float acc = 0.0f;
             if (t > 0) {
-                const float ra = pair0 < len ? ld_l2_f32(rP + c.x) : 0.0f;
-                const float rb = pair0 + 1 < len ? ld_l2_f32(rP + c.z) : 0.0f;
+                const float ra = pair0 < len ? grad_weight<LOGISTIC>(ld_l2_f32(rP + c.x)) : 0.0f;
+                const float rb = pair0 + 1 < len ? grad_weight<LOGISTIC>(ld_l2_f32(rP + c.z)) : 0.0f;
                 acc = fmaf(__int_as_float(c.y), ra, __int_as_float(c.w) * rb);
             }
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gm, acc, o);
             float d = 0.0f;
             if (t == 0) {
-                const float xp = prox_l1(xi, acc, P.beta * __int_as_float(c.x), P.lambda);
+                const float xp = block_step<LOGISTIC>(xi, acc, P.beta * __int_as_float(c.x), P.lambda);
                 d = xp - xi;
                 if (d != 0.0f) {
                     if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
@@ -238,21 +238,32 @@ __global__ void max_len_kernel(int64_t n, const long long* __restrict__ colptr, 
     if ((threadIdx.x & 31) == 0) atomicMax(out, b);
 }
 
-template <int G, bool ONE>
+template <int G, bool ONE, bool LOG>
 cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
     void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel((const void*)pcdm_packed_kernel<G, ONE>, dim3(ctas), dim3(kThreads), args, 0,
-                                       st);
+    return cudaLaunchCooperativeKernel((const void*)pcdm_packed_kernel<G, ONE, LOG>, dim3(ctas), dim3(kThreads),
+                                       args, 0, st);
 }
 
-template <bool ONE>
+template <bool ONE, bool LOG>
 const void* kernel_ptr(int G) {
     switch (G) {
-        case 2: return (const void*)pcdm_packed_kernel<2, ONE>;
-        case 4: return (const void*)pcdm_packed_kernel<4, ONE>;
-        case 8: return (const void*)pcdm_packed_kernel<8, ONE>;
-        case 16: return (const void*)pcdm_packed_kernel<16, ONE>;
-        default: return (const void*)pcdm_packed_kernel<32, ONE>;
+        case 2: return (const void*)pcdm_packed_kernel<2, ONE, LOG>;
+        case 4: return (const void*)pcdm_packed_kernel<4, ONE, LOG>;
+        case 8: return (const void*)pcdm_packed_kernel<8, ONE, LOG>;
+        case 16: return (const void*)pcdm_packed_kernel<16, ONE, LOG>;
+        default: return (const void*)pcdm_packed_kernel<32, ONE, LOG>;
+    }
+}
+
+template <bool ONE, bool LOG>
+cudaError_t launch_sel(int G, int ctas, const PackedParams& P, cudaStream_t st) {
+    switch (G) {
+        case 2: return launch_g<2, ONE, LOG>(ctas, P, st);
+        case 4: return launch_g<4, ONE, LOG>(ctas, P, st);
+        case 8: return launch_g<8, ONE, LOG>(ctas, P, st);
+        case 16: return launch_g<16, ONE, LOG>(ctas, P, st);
+        default: return launch_g<32, ONE, LOG>(ctas, P, st);
     }
 }
 
@@ -314,9 +325,10 @@ cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st,
     return cudaGetLastError();
 }
 
-int packed_ctas(int G, bool one_barrier, int sms) {
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic) {
     int per_sm = 1;
-    const void* fn = one_barrier ? kernel_ptr<true>(G) : kernel_ptr<false>(G);
+    const void* fn = logistic ? (one_barrier ? kernel_ptr<true, true>(G) : kernel_ptr<false, true>(G))
+                              : (one_barrier ? kernel_ptr<true, false>(G) : kernel_ptr<false, false>(G));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     return per_sm * sms;
@@ -325,22 +337,8 @@ int packed_ctas(int G, bool one_barrier, int sms) {
 cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
                           int64_t* launches) {
     ++*launches;
-    if (one_barrier) {
-        switch (G) {
-            case 2: return launch_g<2, true>(ctas, P, st);
-            case 4: return launch_g<4, true>(ctas, P, st);
-            case 8: return launch_g<8, true>(ctas, P, st);
-            case 16: return launch_g<16, true>(ctas, P, st);
-            default: return launch_g<32, true>(ctas, P, st);
-        }
-    }
-    switch (G) {
-        case 2: return launch_g<2, false>(ctas, P, st);
-        case 4: return launch_g<4, false>(ctas, P, st);
-        case 8: return launch_g<8, false>(ctas, P, st);
-        case 16: return launch_g<16, false>(ctas, P, st);
-        default: return launch_g<32, false>(ctas, P, st);
-    }
+    if (P.logistic) return one_barrier ? launch_sel<true, true>(G, ctas, P, st) : launch_sel<false, true>(G, ctas, P, st);
+    return one_barrier ? launch_sel<true, false>(G, ctas, P, st) : launch_sel<false, false>(G, ctas, P, st);
 }
 
 }  // namespace pcdm_internal

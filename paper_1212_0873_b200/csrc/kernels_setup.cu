@@ -187,9 +187,77 @@ __global__ void objective_sums_kernel(int64_t m, int64_t n, const double* __rest
     }
 }
 
+// L2-regularised logistic problem: labels must be +-1; A~ = diag(y) A in place.
+__global__ void check_labels_kernel(int64_t m, const float* __restrict__ y, int* __restrict__ flags) {
+    int bad = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+        if (!(y[t] == 1.0f || y[t] == -1.0f)) bad = FLAG_NONFINITE_B;
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, bad);
+}
+
+__global__ void fold_labels_kernel(int64_t nnz, const int* __restrict__ rowidx, const float* __restrict__ y,
+                                   float* __restrict__ val) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+        val[p] *= y[rowidx[p]];
+}
+
+__global__ void scale_kernel(int64_t n, float a, float* __restrict__ v) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        v[t] *= a;
+}
+
+// out[0] += sum log(1 + exp(-s_j)) (fp64, stable), out[1] += sum x_i^2
+__global__ void objective_logistic_kernel(int64_t m, int64_t n, const double* __restrict__ s64,
+                                          const float* __restrict__ x, double* __restrict__ out) {
+    double a = 0.0, q = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += stride) {
+        const double v = s64[t];
+        a += v >= 0.0 ? log1p(exp(-v)) : -v + log1p(exp(v));
+    }
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const double xv = (double)x[t];
+        q += xv * xv;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, a);
+        atomicAdd(out + 1, q);
+    }
+}
+
 }  // namespace
 
 namespace pcdm_internal {
+
+cudaError_t launch_logistic_setup(int64_t m, int64_t nnz, const int* rowidx, const float* y, float* val, int* flags,
+                                  cudaStream_t st, int sms, int64_t* launches) {
+    check_labels_kernel<<<grid_for(m, kThreads, sms * 8), kThreads, 0, st>>>(m, y, flags);
+    fold_labels_kernel<<<grid_for(nnz, kThreads, sms * 16), kThreads, 0, st>>>(nnz, rowidx, y, val);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(int64_t n, float a, float* v, cudaStream_t st, int sms, int64_t* launches) {
+    scale_kernel<<<grid_for(n, kThreads, sms * 8), kThreads, 0, st>>>(n, a, v);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_objective_logistic(int64_t m, int64_t n, const double* s64, const float* x, double* out,
+                                      cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    objective_logistic_kernel<<<grid_for(m > n ? m : n, kThreads, sms * 4), kThreads, 0, st>>>(m, n, s64, x, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 
 cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches) {
     const int blocks = grid_for(A.n * 32, kThreads, sms * 16);

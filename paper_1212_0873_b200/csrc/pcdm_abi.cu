@@ -74,6 +74,7 @@ struct pcdm_problem {
     int64_t m = 0, n = 0, nnz = 0;
     double lambda = 0.0;
     int64_t omega = 0;
+    int loss = 0;              // 0: LASSO (square loss), 1: L2-regularised logistic
     int64_t* colptr = nullptr;
     int* rowidx = nullptr;
     float* val = nullptr;
@@ -375,6 +376,8 @@ pcdm_status sampling_dev(const SamplingSpec& sp, uint64_t** dev_T, size_t* cap, 
 
 pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_t iters, uint64_t seed,
                      int64_t first_iter, int64_t refresh_every, double beta_override, int32_t variant, void* stream);
+pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
+                        const float* val, const float* b, double lambda, int loss, void* stream, pcdm_problem** out);
 
 }  // namespace
 
@@ -384,6 +387,22 @@ const char* pcdm_last_error(void) { return g_error.c_str(); }
 
 pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
                         const float* val, const float* b, double lambda, void* stream, pcdm_problem** out) {
+    return create_impl(m, n, nnz, colptr, rowidx, val, b, lambda, 0, stream, out);
+}
+
+pcdm_status pcdm_create_logistic(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
+                                 const float* val, const float* y, double lambda, void* stream, pcdm_problem** out) {
+    return create_impl(m, n, nnz, colptr, rowidx, val, y, lambda, 1, stream, out);
+}
+
+}  // extern "C"
+
+namespace {
+
+// loss 0: LASSO with b; loss 1: L2-regularised logistic with labels y (the library
+// stores A~ = diag(y) A, b = 0, L = ||a_i||^2 / 4; R21)
+pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
+                        const float* val, const float* b, double lambda, int loss, void* stream, pcdm_problem** out) {
     if (!out) return fail(PCDM_EINVAL, "out must not be NULL");
     *out = nullptr;
     if (m < 1 || n < 1 || nnz < 1) return fail(PCDM_EINVAL, "need m, n, nnz >= 1 (no loss terms otherwise)");
@@ -396,6 +415,7 @@ pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
     p->n = n;
     p->nnz = nnz;
     p->lambda = lambda;
+    p->loss = loss;
     pcdm_status s = PCDM_OK;
     int64_t launches = 0;
     Scalars hs{};
@@ -405,16 +425,27 @@ pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         if ((s = dev_copy_in(&p->colptr, colptr, (size_t)n + 1, st, "copy colptr")) != PCDM_OK) break;
         if ((s = dev_copy_in(&p->rowidx, rowidx, (size_t)nnz, st, "copy rowidx")) != PCDM_OK) break;
         if ((s = dev_copy_in(&p->val, val, (size_t)nnz, st, "copy val")) != PCDM_OK) break;
-        if ((s = dev_copy_in(&p->b, b, (size_t)m, st, "copy b")) != PCDM_OK) break;
+        if ((s = dev_copy_in(&p->b, b, (size_t)m, st, loss ? "copy y" : "copy b")) != PCDM_OK) break;
         cudaError_t e;
         if ((e = cudaMalloc((void**)&p->sc, sizeof(Scalars))) != cudaSuccess) { s = cuda_fail(e, "scalars"); break; }
         if ((e = cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st)) != cudaSuccess) { s = cuda_fail(e, "memset"); break; }
         if ((e = launch_validate(p->csc(), &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "validate"); break; }
-        if ((e = launch_check_finite(m, p->b, FLAG_NONFINITE_B, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "check b"); break; }
+        if (loss == 0) {
+            if ((e = launch_check_finite(m, p->b, FLAG_NONFINITE_B, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "check b"); break; }
+        } else {
+            // labels +-1 (flagged as FLAG_NONFINITE_B otherwise), A~ = diag(y) A, then b = 0: r holds s = A~ x
+            if ((e = launch_logistic_setup(m, nnz, p->rowidx, p->b, p->val, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "labels"); break; }
+            if ((e = cudaMemsetAsync(p->b, 0, sizeof(float) * m, st)) != cudaSuccess) { s = cuda_fail(e, "memset b"); break; }
+        }
         if ((s = read_scalars(p, &hs, st)) != PCDM_OK) break;
-        if (hs.flags) { s = fail(PCDM_EINVAL, "invalid CSC input: %s", flag_text(hs.flags)); break; }
+        if (hs.flags) {
+            s = fail(PCDM_EINVAL, "invalid input: %s",
+                     (loss && (hs.flags & FLAG_NONFINITE_B)) ? "labels y must be +1 or -1" : flag_text(hs.flags));
+            break;
+        }
         if ((e = cudaMalloc((void**)&p->L, sizeof(float) * n)) != cudaSuccess) { s = cuda_fail(e, "alloc L"); break; }
         if ((e = launch_col_norms(p->csc(), p->L, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "col norms"); break; }
+        if (loss == 1 && (e = launch_scale(n, 0.25f, p->L, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "L"); break; }
         int* counts = nullptr;
         if ((e = cudaMalloc((void**)&counts, sizeof(int) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc counts"); break; }
         e = launch_row_counts(p->csc(), counts, st, p->sms, &launches);
@@ -453,6 +484,10 @@ pcdm_status pcdm_create(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
     *out = p;
     return PCDM_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 void pcdm_destroy(pcdm_problem* p) {
     if (!p) return;
@@ -540,7 +575,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (beta_override > 0.0) beta_d = beta_override;
     const int64_t R = refresh_period(p->n, tau, refresh_every);
     IterLaunch plan = plan_iter(variant == PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
-                                p->sms, p->device);
+                                p->sms, p->device, p->loss == 1);
     // AUTO: packed blocks whenever the shared-memory variant does not apply
     const bool packed = p->packed_G > 0 &&
                         (variant == PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
@@ -555,7 +590,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.variant = PCDM_VARIANT_PACKED;
         plan.lanes = p->packed_G;
         plan.threads = 512;
-        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms);
+        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1);
     }
     if (p->nz_cap < tau) {
         cudaFree(p->nz_idx);
@@ -596,6 +631,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     P.nz_total = &p->sc->nz_total;
     P.m = p->m;
     P.n = p->n;
+    P.logistic = p->loss;
     PackedParams Q{};
     Q.blocks = p->blocks;
     Q.x = xd;
@@ -610,6 +646,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.barrier = &p->sc->barrier;
     Q.flags = &p->sc->flags;
     Q.nz_total = &p->sc->nz_total;
+    Q.logistic = p->loss;
 
     int64_t done = 0;
     while (done < iters) {
@@ -690,6 +727,7 @@ pcdm_status pcdm_run_async(pcdm_problem* p, float* x, int64_t updates, int64_t t
     if (updates < 0 || tau_beta < 0) return fail(PCDM_EINVAL, "updates and tau_beta must be >= 0");
     if (!p->packed_G)
         return fail(PCDM_EINVAL, "asynchronous variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
+    if (p->loss != 0) return fail(PCDM_EINVAL, "asynchronous variant: LASSO problems only");
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
@@ -790,13 +828,18 @@ pcdm_status pcdm_objective(pcdm_problem* p, const float* x, double* F, void* str
         cudaError_t e = cudaMemsetAsync(&p->sc->flags, 0, sizeof(int), st);
         if (e != cudaSuccess) { s = cuda_fail(e, "memset"); break; }
         if ((e = launch_residual64(p->csc(), p->b, xd, p->r64, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "residual"); break; }
-        if ((e = launch_objective_sums(p->m, p->n, p->r64, xd, p->sc->sums, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "objective"); break; }
+        if (p->loss == 0) {
+            if ((e = launch_objective_sums(p->m, p->n, p->r64, xd, p->sc->sums, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "objective"); break; }
+        } else if ((e = launch_objective_logistic(p->m, p->n, p->r64, xd, p->sc->sums, st, p->sms, &launches)) != cudaSuccess) {
+            s = cuda_fail(e, "objective");
+            break;
+        }
         s = read_scalars(p, &hs, st);
     } while (0);
     cudaFree(tmp);
     if (s != PCDM_OK) return s;
     if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
-    *F = 0.5 * hs.sums[0] + p->lambda * hs.sums[1];
+    *F = (p->loss == 0 ? 0.5 * hs.sums[0] : hs.sums[0]) + p->lambda * hs.sums[1];
     return PCDM_OK;
 }
 

@@ -23,7 +23,8 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EDIVERGED", 5
 EXPORTS = ["pcdm_create", "pcdm_destroy", "pcdm_last_error", "pcdm_omega", "pcdm_beta", "pcdm_run",
            "pcdm_run_ex", "pcdm_objective", "pcdm_last_run_stats", "pcdm_sample", "pcdm_col_norms",
            "pcdm_row_counts", "pcdm_residual", "pcdm_philox", "pcdm_philox_check_curand",
-           "pcdm_run_sampling", "pcdm_beta_sampling", "pcdm_sample_sampling", "pcdm_run_async"]
+           "pcdm_run_sampling", "pcdm_beta_sampling", "pcdm_sample_sampling", "pcdm_run_async",
+           "pcdm_create_logistic"]
 SAMPLING_KINDS = {"nice": 0, "independent": 1, "binomial": 2, "du": 3}
 
 
@@ -99,6 +100,7 @@ def load():
         "pcdm_philox_check_curand": ([i64, u64, ctypes.POINTER(i64), P], st),
         "pcdm_run_sampling": ([P, P, ctypes.POINTER(_CSampling), i64, u64, i64, i64, f64, i32, P], st),
         "pcdm_run_async": ([P, P, i64, i64, f64, i64, u64, u64, P], st),
+        "pcdm_create_logistic": ([i64, i64, i64, P, P, P, P, f64, P, ctypes.POINTER(P)], st),
         "pcdm_beta_sampling": ([P, ctypes.POINTER(_CSampling), ctypes.POINTER(f64)], st),
         "pcdm_sample_sampling": ([i64, ctypes.POINTER(_CSampling), u64, i64, i64, P, P], st),
     }
@@ -155,6 +157,15 @@ def pcdm_create(m, n, colptr, rowidx, val, b, lam, stream=None):
     _check(load().pcdm_create(int(m), int(n), nnz, _ptr(colptr, "i64"), _ptr(rowidx, "i32"),
                               _ptr(val, "f32"), _ptr(b, "f32"), float(lam), _stream(stream),
                               ctypes.byref(h)))
+    return h
+
+
+def pcdm_create_logistic(m, n, colptr, rowidx, val, y, lam, stream=None):
+    nnz = int(rowidx.shape[0]) if hasattr(rowidx, "shape") else len(rowidx)
+    h = ctypes.c_void_p()
+    _check(load().pcdm_create_logistic(int(m), int(n), nnz, _ptr(colptr, "i64"), _ptr(rowidx, "i32"),
+                                       _ptr(val, "f32"), _ptr(y, "f32"), float(lam), _stream(stream),
+                                       ctypes.byref(h)))
     return h
 
 
@@ -263,9 +274,16 @@ def pcdm_philox_check_curand(count, seed, stream=None) -> int:
 class Problem:
     """Owning wrapper around a pcdm_problem handle (destroyed on close / GC)."""
 
-    def __init__(self, m, n, colptr, rowidx, val, b, lam, stream=None):
+    def __init__(self, m, n, colptr, rowidx, val, b, lam, stream=None, loss="lasso"):
+        """loss "lasso": b is the target; loss "logistic": b holds the labels y (+-1)."""
         self.m, self.n, self.nnz, self.lam = int(m), int(n), int(rowidx.shape[0]), float(lam)
-        self.handle = pcdm_create(m, n, colptr, rowidx, val, b, lam, stream)
+        self.loss = loss
+        if loss == "lasso":
+            self.handle = pcdm_create(m, n, colptr, rowidx, val, b, lam, stream)
+        elif loss == "logistic":
+            self.handle = pcdm_create_logistic(m, n, colptr, rowidx, val, b, lam, stream)
+        else:
+            raise ValueError("loss must be 'lasso' or 'logistic'")
 
     @classmethod
     def from_instance(cls, inst, stream=None):
