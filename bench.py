@@ -43,8 +43,9 @@ VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", -1: "async"}
 KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
                      -1: "pcdm_async_kernel"}
 # oracle iterations per reference step / cpu_baseline sample, per config
-REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4}
-CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24}
+REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4, "logistic_small": 200, "kddb_like": 4}
+CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24, "logistic_small": 1000,
+                      "kddb_like": 24}
 
 
 def parse():
@@ -53,7 +54,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="huge", choices=list(I.CONFIGS))
+    ap.add_argument("--config", default=None, choices=list(I.CONFIGS) + list(I.LOGISTIC_CONFIGS),
+                    help="default: huge (LASSO) / kddb_like (logistic)")
+    ap.add_argument("--loss", default="lasso", choices=["lasso", "logistic"],
+                    help="logistic: the L2-regularised logistic problem of Sec. 8.4 (NEXT-3)")
     ap.add_argument("--tau", type=int, default=None)
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--variant", default="auto")
@@ -64,7 +68,33 @@ def parse():
                     help="asynchronous variant (NEXT-4, PAPER.md:1248): tau*iters updates per step, no barriers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.config is None:
+        a.config = "kddb_like" if a.loss == "logistic" else "huge"
+    return a
+
+
+class LogisticInstance:
+    """The synthetic KDDB-shaped logistic instance in the shape bench.py uses (b = labels y)."""
+
+    def __init__(self, cfg, device):
+        self.cfg = I.LOGISTIC_CONFIGS[cfg] if isinstance(cfg, str) else cfg
+        self.colptr, self.rowidx, self.val, self.b, self.lam = I.generate_logistic(self.cfg, seed=0, device=device)
+        self.m, self.n = self.cfg.m, self.cfg.n
+
+    @property
+    def nnz(self):
+        return int(self.rowidx.numel())
+
+
+def make_instance(args, device):
+    if args.loss == "logistic":
+        return LogisticInstance(args.config, device)
+    return I.generate(I.CONFIGS[args.config], seed=0, device=device)
+
+
+def config_of(args):
+    return I.LOGISTIC_CONFIGS[args.config] if args.loss == "logistic" else I.CONFIGS[args.config]
 
 
 # ----------------------------------------------------------------------------- dist
@@ -223,12 +253,15 @@ def oracle_subinstance(inst, tau, k0, k_iters, seed, osamp=None):
     return full, rows, vals, inst.b.cpu().numpy()
 
 
-def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None, osamp=None):
+def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None, osamp=None, loss="lasso"):
     import oracle
     if sub is None:
         sub = oracle_subinstance(inst, tau, k0, k_iters, seed, osamp)
     c, r, v, b = sub
-    res = oracle.run(inst.m, c, r, v, b, inst.lam, tau, k_iters, seed, first_iter=k0, sampling=osamp)
+    if loss == "logistic":
+        res = oracle.logistic_run(inst.m, c, r, v, b, inst.lam, tau, k_iters, seed, first_iter=k0, sampling=osamp)
+    else:
+        res = oracle.run(inst.m, c, r, v, b, inst.lam, tau, k_iters, seed, first_iter=k0, sampling=osamp)
     return res.loop_seconds, sub
 
 
@@ -236,18 +269,18 @@ def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None, osamp=None):
 def bench_reference(args, world, rank):
     if rank != 0:
         return
-    cfg = I.CONFIGS[args.config]
+    cfg = config_of(args)
     tau = args.tau or cfg.tau
     kref = REF_ITERS[args.config]
     dev = torch.device("cuda", 0)
-    inst = I.generate(cfg, seed=0, device=dev)
+    inst = make_instance(args, dev)
     K, W = args.steps, args.warmup
     osamp = oracle_sampling(args, tau)
     sub = oracle_subinstance(inst, tau, 0, kref * (K + W), seed=0, osamp=osamp)
     del inst.rowidx, inst.val
     secs = []
     for s in range(W + K):
-        t, _ = run_oracle_sample(inst, tau, s * kref, kref, 0, sub=sub, osamp=osamp)
+        t, _ = run_oracle_sample(inst, tau, s * kref, kref, 0, sub=sub, osamp=osamp, loss=args.loss)
         if s >= W:
             secs.append(t)
     step_s = sum(secs) / len(secs)
@@ -273,7 +306,7 @@ def bench_ours(args, world, rank, local):
         pbuild.build()
     barrier(world)
     pcdm.load()
-    cfg = I.CONFIGS[args.config]
+    cfg = config_of(args)
     tau = args.tau or cfg.tau
     iters = args.iters or cfg.iters
     K, W = args.steps, args.warmup
@@ -281,11 +314,11 @@ def bench_ours(args, world, rank, local):
     stream = torch.cuda.current_stream(dev)
 
     t0 = time.time()
-    inst = I.generate(cfg, seed=0, device=dev)
+    inst = make_instance(args, dev)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     t0 = time.time()
-    prob = pcdm.Problem.from_instance(inst)
+    prob = pcdm.Problem(inst.m, inst.n, inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, loss=args.loss)
     create_s = time.time() - t0
     nnz = inst.nnz
     avg_c = nnz / inst.n
@@ -378,7 +411,7 @@ def bench_ours(args, world, rank, local):
 
     cpu = None
     if do_cpu:
-        secs, _ = run_oracle_sample(inst, tau, 0, kcpu, 0, sub=sub, osamp=osamp)
+        secs, _ = run_oracle_sample(inst, tau, 0, kcpu, 0, sub=sub, osamp=osamp, loss=args.loss)
         cpu = {"value": size * kcpu / secs, "unit": "updates/s", "cores": 1, "kind": "oracle",
                "sample": "iterations k=0..%d of the %s run (tau=%d) on the columns they touch; "
                          "O5-O8 loop time %.2f s" % (kcpu - 1, cfg.name, tau, secs)}
@@ -391,7 +424,7 @@ def bench_ours(args, world, rank, local):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "nnz": nnz, "nnz_per_col": cfg.nnz_per_col,
-                   "rows": cfg.rows, "tau": tau, "iters_per_step": iters, "seed_instance": 0,
+                   "rows": cfg.rows, "tau": tau, "iters_per_step": iters, "seed_instance": 0, "loss": args.loss,
                    "sampling": args.sampling if args.sampling != "binomial" else "binomial(p_b=%g)" % args.p_b,
                    "seed_run": "rank", "parallelism": "replicas" if world > 1 else "single",
                    "l2": ("inputs larger than L2 (A %.1f GB vs L2 %.0f MB)" % (nnz * 8 / 1e9, l2_bytes / 1e6))
