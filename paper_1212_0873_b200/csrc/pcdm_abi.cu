@@ -581,12 +581,18 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                         (variant == PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
     bool one_barrier = false;
     if (packed) {
-        int l2 = 0;
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
-        one_barrier = 2 * 4 * p->m <= l2 / 4;
+        // one barrier per iteration (double-buffered r, the previous iteration's steps
+        // replayed): measured faster on every config (huge: 45.7 -> 44.2 ms/step,
+        // profiles/r01_one_barrier_huge_ab.log); two barriers if the second buffer
+        // cannot be allocated or PCDM_ONE_BARRIER=0
+        one_barrier = true;
         const char* ob = getenv("PCDM_ONE_BARRIER");
         if (ob) one_barrier = atoi(ob) != 0;
-        if (one_barrier && !p->r2) CK(cudaMalloc((void**)&p->r2, sizeof(float) * p->m), "alloc r2");
+        if (one_barrier && !p->r2 && cudaMalloc((void**)&p->r2, sizeof(float) * p->m) != cudaSuccess) {
+            cudaGetLastError();
+            p->r2 = nullptr;
+            one_barrier = false;
+        }
         plan.variant = PCDM_VARIANT_PACKED;
         plan.lanes = p->packed_G;
         plan.threads = 512;
