@@ -19,8 +19,17 @@ cudaError_t launch_check_finite(int64_t count, const float* v, int flag_bit, int
 cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_max(int64_t count, const int* v, int* out, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms, int64_t* launches);
+// x in the packed block headers (kernels_packed.cu): the residual pass also copies every
+// nonzero x_i into its header and appends i to the dirty list
+struct XHeaders {
+    int4* blocks;
+    int G;
+    int* list;
+    unsigned long long* count;
+    int64_t cap;
+};
 cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
-                              cudaStream_t st, int sms, int64_t* launches);
+                              cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh = nullptr);
 cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,
                            int64_t* launches);
 cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
@@ -97,7 +106,7 @@ struct IterLaunch {
 
 // ---- packed-block hot loop (kernels_packed.cu)
 struct PackedParams {
-    const int4* blocks;   // [n][G] 16-byte chunks: {L, len, 0, 0}, then (row, val) pairs
+    int4* blocks;         // [n][G] 16-byte chunks: {L, len, x (xlist), 0}, then (row, val) pairs
     float* x;
     float* r0;            // residual buffer (TWO_BARRIER: the residual)
     float* r1;            // second buffer (ONE_BARRIER only)
@@ -114,7 +123,15 @@ struct PackedParams {
     int* flags;
     unsigned long long* nz_total;
     int logistic;         // 1: L2-regularised logistic loss (margins in r0/r1)
+    int* xlist;           // non-null: x lives in the block headers; dirty list D of changed i
+    unsigned long long* xlist_count;
+    int64_t xlist_cap;
 };
+cudaError_t launch_xhdr_clear(int4* blocks, int G, const int* list, const unsigned long long* count, int64_t cap,
+                              int64_t n, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_xhdr_out(const int4* blocks, int G, float* x, int64_t n, const int* list,
+                            const unsigned long long* count, int64_t cap, cudaStream_t st, int sms,
+                            int64_t* launches);
 // asynchronous variant (NEXT-4): no barriers, no sampler pass
 struct AsyncParams {
     const int4* blocks;

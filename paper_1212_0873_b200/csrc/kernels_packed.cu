@@ -38,6 +38,13 @@ namespace {
 
 constexpr int kThreads = 512;
 
+// L2 (coherent) 16-byte load: column blocks whose header holds the mutable x_i
+__device__ __forceinline__ int4 ld_l2_v4(const int4* p) {
+    int4 v;
+    asm volatile("ld.global.cg.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
     int4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
@@ -86,8 +93,11 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
             const int i = ld_stream_s32(S + j);
             if (i < 0) continue;  // idle processor (non-nice samplings)
             float xi = 0.0f;
-            if (t == 0) xi = ld_l2_f32(P.x + i);
-            const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+            // x_i lives in the block header (chunk 0 .z) when P.xlist: the column's single
+            // line brings it, no separate random x line; the header is then mutable, so
+            // the block is read through L2 (ld.cg) instead of the non-coherent path
+            const int4 c = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i * G + t) : ld_stream_v4(P.blocks + (int64_t)i * G + t);
+            if (t == 0) xi = P.xlist ? __int_as_float(c.z) : ld_l2_f32(P.x + i);
             const int len = __shfl_sync(gm, c.y, src);
             float acc = 0.0f;
             if (t > 0) {
@@ -103,7 +113,13 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
                 d = xp - xi;
                 if (d != 0.0f) {
                     if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
-                    P.x[i] = xp;
+                    if (P.xlist) {
+                        ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
+                        const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
+                        if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = i;
+                    } else {
+                        P.x[i] = xp;
+                    }
                     const int pos = atomicAdd(P.nz_count + cur, 1);
                     P.nz_idx[cur * tau + pos] = i;
                     P.nz_delta[cur * tau + pos] = d;
@@ -206,6 +222,37 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_async_kernel(AsyncParams A) 
     if (nz) atomicAdd(A.nz_total, nz);
 }
 
+// ---------------------------------------------------------------- x in the block headers
+// The run keeps x_i in chunk 0 .z of column i's block.  The dirty list D (indices
+// whose header may be nonzero; duplicates allowed) ties the headers to the
+// caller's x:  run start: headers of D zeroed, D cleared, every nonzero x_i copied
+// into its header and appended to D (by the residual pass, kernels_setup.cu);
+// during the run every changed i is appended;
+// refresh / run end: x_i = header for i in D.  If D overflows its capacity the
+// start / end passes walk all n columns instead.
+__global__ void xhdr_clear_kernel(int4* __restrict__ blocks, int G, const int* __restrict__ list,
+                                  const unsigned long long* __restrict__ count, int64_t cap, int64_t n) {
+    const unsigned long long c = *count;
+    const bool all = c > (unsigned long long)cap;
+    const int64_t total = all ? n : (int64_t)c;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = all ? t : list[t];
+        ((float*)(blocks + i * G))[2] = 0.0f;
+    }
+}
+
+__global__ void xhdr_out_kernel(const int4* __restrict__ blocks, int G, float* __restrict__ x, int64_t n,
+                                const int* __restrict__ list, const unsigned long long* __restrict__ count,
+                                int64_t cap) {
+    const unsigned long long c = *count;
+    const bool all = c > (unsigned long long)cap;
+    const int64_t total = all ? n : (int64_t)c;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = all ? t : list[t];
+        x[i] = __ldcg((const float*)(blocks + i * G) + 2);
+    }
+}
+
 // Pack the CSC into blocks: one thread per (column, chunk).
 __global__ void pack_kernel(int64_t n, int G, const long long* __restrict__ colptr, const int* __restrict__ rowidx,
                             const float* __restrict__ val, const float* __restrict__ L, int4* __restrict__ blocks) {
@@ -270,6 +317,21 @@ cudaError_t launch_sel(int G, int ctas, const PackedParams& P, cudaStream_t st) 
 }  // namespace
 
 namespace pcdm_internal {
+
+cudaError_t launch_xhdr_clear(int4* blocks, int G, const int* list, const unsigned long long* count, int64_t cap,
+                              int64_t n, cudaStream_t st, int sms, int64_t* launches) {
+    xhdr_clear_kernel<<<sms * 8, 256, 0, st>>>(blocks, G, list, count, cap, n);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xhdr_out(const int4* blocks, int G, float* x, int64_t n, const int* list,
+                            const unsigned long long* count, int64_t cap, cudaStream_t st, int sms,
+                            int64_t* launches) {
+    xhdr_out_kernel<<<sms * 8, 256, 0, st>>>(blocks, G, x, n, list, count, cap);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 int packed_lanes(int64_t max_len) {
     const int64_t chunks = 1 + (max_len + 1) / 2;

@@ -10,6 +10,7 @@
 #include "internal.h"
 
 using namespace pcdm;
+using pcdm_internal::XHeaders;
 
 namespace {
 
@@ -112,11 +113,16 @@ __global__ void neg_b_kernel(int64_t m, const float* __restrict__ b, double* __r
 // thread per 4 columns for the (rare) nonzero ones.
 __device__ __forceinline__ void scatter_col(int64_t i, float xi, const long long* __restrict__ colptr,
                                             const int* __restrict__ rowidx, const float* __restrict__ val,
-                                            double* __restrict__ r64, int& bad) {
+                                            double* __restrict__ r64, int& bad, const XHeaders& xh) {
     if (xi == 0.0f) return;
     if (!isfinite(xi)) {
         bad = FLAG_NONFINITE_X;
         return;
+    }
+    if (xh.blocks) {
+        ((float*)(xh.blocks + i * xh.G))[2] = xi;
+        const unsigned long long q = atomicAdd(xh.count, 1ull);
+        if (q < (unsigned long long)xh.cap) xh.list[q] = (int)i;
     }
     const double xd = (double)xi;
     for (long long p = colptr[i]; p < colptr[i + 1]; ++p) atomicAdd(r64 + rowidx[p], (double)val[p] * xd);
@@ -125,21 +131,21 @@ __device__ __forceinline__ void scatter_col(int64_t i, float xi, const long long
 __global__ void scatter_x_kernel(int64_t n, const long long* __restrict__ colptr,
                                  const int* __restrict__ rowidx, const float* __restrict__ val,
                                  const float* __restrict__ x, double* __restrict__ r64,
-                                 int* __restrict__ flags) {
+                                 int* __restrict__ flags, XHeaders xh) {
     int bad = 0;
     const int64_t n4 = ((uintptr_t)x % 16 == 0) ? n / 4 : 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
         const float4 v = __ldcs((const float4*)x + q);
         if (v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f) {
-            scatter_col(4 * q, v.x, colptr, rowidx, val, r64, bad);
-            scatter_col(4 * q + 1, v.y, colptr, rowidx, val, r64, bad);
-            scatter_col(4 * q + 2, v.z, colptr, rowidx, val, r64, bad);
-            scatter_col(4 * q + 3, v.w, colptr, rowidx, val, r64, bad);
+            scatter_col(4 * q, v.x, colptr, rowidx, val, r64, bad, xh);
+            scatter_col(4 * q + 1, v.y, colptr, rowidx, val, r64, bad, xh);
+            scatter_col(4 * q + 2, v.z, colptr, rowidx, val, r64, bad, xh);
+            scatter_col(4 * q + 3, v.w, colptr, rowidx, val, r64, bad, xh);
         }
     }
     for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        scatter_col(i, x[i], colptr, rowidx, val, r64, bad);
+        scatter_col(i, x[i], colptr, rowidx, val, r64, bad, xh);
     bad = __reduce_or_sync(0xffffffffu, bad);
     if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, bad);
 }
@@ -301,10 +307,11 @@ cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms
 }
 
 cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
-                              cudaStream_t st, int sms, int64_t* launches) {
+                              cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh) {
+    const XHeaders none{nullptr, 0, nullptr, nullptr, 0};
     neg_b_kernel<<<grid_for(A.m, kThreads, sms * 8), kThreads, 0, st>>>(A.m, b, r64);
     scatter_x_kernel<<<grid_for((A.n + 3) / 4, kThreads, sms * 8), kThreads, 0, st>>>(
-        A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags);
+        A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags, xh ? *xh : none);
     *launches += 2;
     return cudaGetLastError();
 }

@@ -84,6 +84,9 @@ struct pcdm_problem {
     float* r2 = nullptr;       // second residual buffer (one-barrier packed loop)
     float* r_cur = nullptr;    // buffer holding the residual after the last run
     int4* blocks = nullptr;    // packed column blocks (PACKED variant), [n][packed_G]
+    int* xlist = nullptr;      // dirty list D of columns whose block header may hold x_i != 0
+    unsigned long long* xlist_count = nullptr;  // |D| (> cap: overflowed, walk all n)
+    int64_t xlist_cap = 0;
     int packed_G = 0;          // 0: no packed copy (a column longer than 62 entries)
     int64_t max_len = 0;
     double* r64 = nullptr;
@@ -122,6 +125,8 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->r64);
     cudaFree(p->r2);
     cudaFree(p->blocks);
+    cudaFree(p->xlist);
+    cudaFree(p->xlist_count);
     cudaFree(p->xbuf);
     cudaFree(p->sc);
     cudaFree(p->nz_idx);
@@ -149,8 +154,9 @@ pcdm_status read_scalars(pcdm_problem* p, Scalars* host, cudaStream_t st) {
 }
 
 // r <- A x - b with fp64 accumulation (x device pointer).
-pcdm_status residual_from(pcdm_problem* p, const float* x, cudaStream_t st, int64_t* launches) {
-    CK(launch_residual64(p->csc(), p->b, x, p->r64, &p->sc->flags, st, p->sms, launches), "residual kernels");
+pcdm_status residual_from(pcdm_problem* p, const float* x, cudaStream_t st, int64_t* launches,
+                          const XHeaders* xh = nullptr) {
+    CK(launch_residual64(p->csc(), p->b, x, p->r64, &p->sc->flags, st, p->sms, launches, xh), "residual kernels");
     CK(launch_round_r(p->m, p->r64, p->r, st, p->sms, launches), "residual rounding");
     return PCDM_OK;
 }
@@ -564,12 +570,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         xd = p->xbuf;
     }
     CK(cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st), "memset scalars");
-    pcdm_status s = residual_from(p, xd, st, &launches);
-    if (s != PCDM_OK) return s;
-    CK(tm.end(T_SETUP, t0), "event");
+    pcdm_status s = PCDM_OK;
     Scalars hs{};
-    if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
-    if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
 
     double beta_d = sampling_beta(spec, p->omega, p->n);
     if (beta_override > 0.0) beta_d = beta_override;
@@ -608,7 +610,39 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(cudaMalloc((void**)&p->nz_delta, sizeof(float) * 3 * tau), "alloc step list");
         p->nz_cap = tau;
     }
+    // x in the block headers (packed loop): saves the separate random x line of every
+    // update; PCDM_X_IN_BLOCK=0 keeps x in the caller's array.  The start-of-run
+    // header load rides on the residual pass, which reads x anyway.
+    const char* xib = getenv("PCDM_X_IN_BLOCK");
+    const bool xhdr = packed && !(xib && atoi(xib) == 0);
+    XHeaders xh{};
+    if (xhdr) {
+        if (!p->xlist) {
+            int64_t cap = std::min<int64_t>(p->n, (int64_t)1 << 26);
+            if (const char* xc = getenv("PCDM_XLIST_CAP")) cap = std::max<int64_t>(1, atoll(xc));
+            CK(cudaMalloc((void**)&p->xlist, sizeof(int) * cap), "alloc x list");
+            CK(cudaMalloc((void**)&p->xlist_count, sizeof(unsigned long long)), "alloc x list");
+            CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
+            p->xlist_cap = cap;
+        }
+        CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap, p->n, st, p->sms,
+                             &launches),
+           "x headers");
+        CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
+        xh = XHeaders{p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap};
+    }
+    if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr)) != PCDM_OK) return s;
     if (one_barrier) CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
+    CK(tm.end(T_SETUP, t0), "event");
+    if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
+    if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
+    auto x_out = [&]() -> pcdm_status {
+        if (xhdr)
+            CK(launch_xhdr_out(p->blocks, p->packed_G, xd, p->n, p->xlist, p->xlist_count, p->xlist_cap, st, p->sms,
+                               &launches),
+               "x headers");
+        return PCDM_OK;
+    };
     int64_t chunk = choose_chunk(p->n, tau, iters);
     if (R > 0) chunk = std::min(chunk, R);
     SamplerPlan sp;
@@ -653,6 +687,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.flags = &p->sc->flags;
     Q.nz_total = &p->sc->nz_total;
     Q.logistic = p->loss;
+    Q.xlist = xhdr ? p->xlist : nullptr;
+    Q.xlist_count = p->xlist_count;
+    Q.xlist_cap = p->xlist_cap;
 
     int64_t done = 0;
     while (done < iters) {
@@ -685,6 +722,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         if (R > 0 && done % R == 0) {
             int tr;
             CK(tm.begin(&tr), "event");
+            if ((s = x_out()) != PCDM_OK) return s;  // the refresh reads x
             if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) return s;
             if (one_barrier) {
                 CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
@@ -697,6 +735,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     p->r_cur = (one_barrier && (iters & 1)) ? p->r2 : p->r;
     int tx;
     CK(tm.begin(&tx), "event");
+    if ((s = x_out()) != PCDM_OK) return s;
     if (!x_dev) CK(cudaMemcpyAsync(x, p->xbuf, sizeof(float) * p->n, cudaMemcpyDeviceToHost, st), "copy x out");
     CK(tm.end(T_SETUP, tx), "event");
     int rmax = 0;

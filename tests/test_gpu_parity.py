@@ -336,3 +336,38 @@ def test_sampling_errors(gpu):
             prob.run(x, 0, 1, sampling=bad)
         assert e.value.status == pcdm.PCDM_EINVAL
     prob.close()
+
+
+# ------------------------------------------------------------------ x in the block headers (packed loop)
+@pytest.mark.parametrize("mode", [("1", None), ("0", None), ("1", "5")], ids=["hdr", "array", "hdr-overflow"])
+def test_x_in_block_headers(gpu, monkeypatch, mode):
+    monkeypatch.setenv("PCDM_X_IN_BLOCK", mode[0])
+    if mode[1]:
+        monkeypatch.setenv("PCDM_XLIST_CAP", mode[1])  # tiny dirty list: start / end passes walk all columns
+    m, n = 4000, 3000
+    c, r, v, b, lam = _ragged(m, n, np.random.default_rng(4).integers(1, 40, size=n), 41)
+    x0 = np.random.default_rng(5).normal(size=n) * (np.arange(n) % 3 == 0)
+    for tau, iters, refresh in ((64, 150, 0), (1500, 30, 7), (3000, 6, -1)):
+        out = run_both(c, r, v, b, lam, m, tau, iters, seed=tau, variant="packed", x0=x0, refresh_every=refresh)
+        assert_parity(out)
+
+
+def test_caller_changes_x_between_runs(gpu):
+    # the library must take the caller's x afresh at every run (headers are re-synchronised)
+    m, n = 3000, 2000
+    c, r, v, b, lam = _ragged(m, n, np.full(n, 12), 42)
+    prob = pcdm.Problem(m, n, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), lam)
+    x = torch.zeros(n, device=gpu)
+    prob.run(x, 128, 200, seed=1, variant="packed")
+    x1 = np.random.default_rng(6).normal(size=n) * (np.arange(n) % 5 == 1)
+    x.copy_(torch.from_numpy(x1.astype(np.float32)))
+    prob.run(x, 128, 100, seed=2, first_iter=200, variant="packed")
+    xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), lam, 128, 100, 2, first_iter=200,
+                    x0=x1.astype(np.float32).astype(np.float64)).x
+    assert np.max(np.abs(to_host(x) - xo)) <= 1e-4 * np.max(np.abs(xo))
+    # and a zero x after a run with a big support
+    x.zero_()
+    prob.run(x, 128, 50, seed=3, variant="packed")
+    xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), lam, 128, 50, 3).x
+    assert np.max(np.abs(to_host(x) - xo)) <= 1e-4 * np.max(np.abs(xo))
+    prob.close()
