@@ -114,6 +114,10 @@ typedef struct {
     double iter_kernel_ms;      /* summed device time of the iteration kernel       */
     double sampler_ms;          /* summed device time of the sampler passes         */
     double setup_ms;            /* residual init/refresh + copies (device time)     */
+    int64_t hot_rows;           /* PACKED: rows served from the per-CTA shared-memory
+                                   copy of r (rows stored >= max(64, 32 x mean) times,
+                                   the 2048 most frequent; 0 for uniform rows, and 0
+                                   when tau x (count of the hottest row) < 1024 n)    */
 } pcdm_run_stats;
 
 /* pcdm_create -- build a problem handle for LASSO with A (m x n, CSC), b, lambda.

@@ -18,6 +18,9 @@ cudaError_t launch_check_finite(int64_t count, const float* v, int flag_bit, int
                                 int sms, int64_t* launches);
 cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_max(int64_t count, const int* v, int* out, cudaStream_t st, int sms, int64_t* launches);
+// rows with counts[j] >= threshold -> (rows, cnts)[0 .. min(*n_out, cap)), *n_out = all of them
+cudaError_t launch_hot_candidates(int64_t m, const int* counts, int threshold, int* rows, int* cnts, int* n_out,
+                                  int cap, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms, int64_t* launches);
 // x in the packed block headers (kernels_packed.cu): the residual pass also copies every
 // nonzero x_i into its header and appends i to the dirty list
@@ -126,6 +129,10 @@ struct PackedParams {
     int* xlist;           // non-null: x lives in the block headers; dirty list D of changed i
     unsigned long long* xlist_count;
     int64_t xlist_cap;
+    const int* hot_rows;  // [nhot] ascending row ids of the hot rows (block row field 0x80000000 | h)
+    int nhot;             // 0: no hot rows (blocks hold plain row ids)
+    int hot_cache;        // 1: copy r_k[hot_rows] into shared memory every iteration (else
+                          //    hot entries are gathered through the row table)
 };
 cudaError_t launch_xhdr_clear(int4* blocks, int G, const int* list, const unsigned long long* count, int64_t cap,
                               int64_t n, cudaStream_t st, int sms, int64_t* launches);
@@ -146,16 +153,19 @@ struct AsyncParams {
     float lambda;
     int* flags;
     unsigned long long* nz_total;
+    const int* hot_rows;  // decodes hot-row entries of the blocks (see PackedParams)
 };
 int async_groups(int G, int sms, int* ctas);
 cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st, int64_t* launches);
 int packed_lanes(int64_t max_len);
 cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStream_t st, int sms, int64_t* launches);
+// rows listed in hot_rows[0..nhot) (ascending) are stored as 0x80000000 | h
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
-                        int4* blocks, cudaStream_t st, int sms, int64_t* launches);
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false);
+                        const int* hot_rows, int nhot, int4* blocks, cudaStream_t st, int sms, int64_t* launches);
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false, int nhot = 0);
 cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
                           int64_t* launches);
+size_t packed_smem_bytes(int nhot);
 
 // Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
 IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,

@@ -25,6 +25,15 @@
 //                into Q, so after ONE barrier Q = r_{k-1} + Delta_{k-1} + Delta_k
 //                = r_{k+1} and the buffers swap.  Used when 2 r fits in L2.
 // Step lists rotate over 3 buffers (append k%3, replay (k-1)%3, reset (k+1)%3).
+//
+// Hot rows (skewed row distributions, e.g. the Zipf config): a row stored in a
+// large fraction of the columns is read by that fraction of all sampled columns
+// every iteration, and same-address L2 requests serialise in one L2 slice.  The
+// rows stored >= a threshold times (chosen at create from the row histogram) are
+// encoded in the blocks as 0x80000000 | h; every CTA with work copies
+// r_k[hot_rows[h]] into shared memory at the start of the iteration (r_k is
+// read-only during iteration k in both barrier schemes) and gathers hot entries
+// from there; scatters go to the real row hot_rows[h].
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -63,10 +72,20 @@ __device__ __forceinline__ unsigned gmask_of() {
     }
 }
 
+// real row of a block entry (hot rows stored as 0x80000000 | h)
+__device__ __forceinline__ int real_row(int v, const int* hrow) { return v < 0 ? hrow[v & 0x7fffffff] : v; }
+
 // r[row] += val * d for this lane's (<= 2) pairs of the chunk.
-__device__ __forceinline__ void scatter_chunk(float* r, const int4 c, int pair0, int len, float d) {
-    if (pair0 < len) red_add_f32(r + c.x, __int_as_float(c.y) * d);
-    if (pair0 + 1 < len) red_add_f32(r + c.z, __int_as_float(c.w) * d);
+__device__ __forceinline__ void scatter_chunk(float* r, const int4 c, int pair0, int len, float d, const int* hrow) {
+    if (pair0 < len) red_add_f32(r + real_row(c.x, hrow), __int_as_float(c.y) * d);
+    if (pair0 + 1 < len) red_add_f32(r + real_row(c.z, hrow), __int_as_float(c.w) * d);
+}
+
+// gathered r entry (hot rows from the shared-memory copy, or through the row table
+// when the run does not cache them)
+__device__ __forceinline__ float gather_r(const float* rP, int v, const float* s_hot, const int* s_hrow, bool cache) {
+    if (v >= 0) return ld_l2_f32(rP + v);
+    return cache ? s_hot[v & 0x7fffffff] : ld_l2_f32(rP + s_hrow[v & 0x7fffffff]);
 }
 
 template <int G, bool ONE_BARRIER, bool LOGISTIC>
@@ -79,6 +98,17 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
     const int pair0 = 2 * (t - 1);
     unsigned bar_target = 0;
     const int64_t tau = P.tau;
+    extern __shared__ float s_dyn[];
+    float* s_hot = s_dyn;                      // [nhot] r_k at the hot rows
+    int* s_hrow = (int*)(s_dyn + P.nhot);      // [nhot] hot row ids
+    const int nhot = P.nhot;
+    const bool cache = P.hot_cache != 0;
+    // CTAs without slots in an iteration skip the hot-row copy
+    const bool has_slots = (int64_t)blockIdx.x * (kThreads / G) < tau;
+    if (nhot) {
+        for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
+        __syncthreads();
+    }
 
     for (int64_t it = 0; it < P.iters; ++it) {
         const int64_t k = P.k0 + it;
@@ -87,6 +117,11 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
         float* rQ = (ONE_BARRIER && (k & 1)) ? P.r0 : P.r1;
         const int* S = P.slots + it * tau;
         if (blockIdx.x == 0 && threadIdx.x == 0) P.nz_count[next] = 0;
+        if (cache && has_slots) {
+            // the previous iteration's readers of s_hot passed the grid barrier's __syncthreads
+            for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hot[h] = ld_l2_f32(rP + s_hrow[h]);
+            __syncthreads();
+        }
 
         // ---------------- phase A: one coalesced block load + <= 2 gathers per lane
         for (int64_t j = gid; j < tau; j += ngroups) {
@@ -101,8 +136,8 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
             const int len = __shfl_sync(gm, c.y, src);
             float acc = 0.0f;
             if (t > 0) {
-                const float ra = pair0 < len ? grad_weight<LOGISTIC>(ld_l2_f32(rP + c.x)) : 0.0f;
-                const float rb = pair0 + 1 < len ? grad_weight<LOGISTIC>(ld_l2_f32(rP + c.z)) : 0.0f;
+                const float ra = pair0 < len ? grad_weight<LOGISTIC>(gather_r(rP, c.x, s_hot, s_hrow, cache)) : 0.0f;
+                const float rb = pair0 + 1 < len ? grad_weight<LOGISTIC>(gather_r(rP, c.z, s_hot, s_hrow, cache)) : 0.0f;
                 acc = fmaf(__int_as_float(c.y), ra, __int_as_float(c.w) * rb);
             }
 #pragma unroll
@@ -127,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
             }
             if (ONE_BARRIER) {
                 d = __shfl_sync(gm, d, src);
-                if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d);
+                if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
             }
         }
         if (ONE_BARRIER) {
@@ -138,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
                 const float d = ld_l2_f32(P.nz_delta + prev * tau + e);
                 const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
                 const int len = __shfl_sync(gm, c.y, src);
-                if (t > 0) scatter_chunk(rQ, c, pair0, len, d);
+                if (t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
             }
             grid_barrier(P.barrier, bar_target);
         } else {
@@ -149,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
                 const float d = ld_l2_f32(P.nz_delta + cur * tau + e);
                 const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
                 const int len = __shfl_sync(gm, c.y, src);
-                if (t > 0) scatter_chunk(P.r0, c, pair0, len, d);
+                if (t > 0) scatter_chunk(P.r0, c, pair0, len, d, s_hrow);
             }
             grid_barrier(P.barrier, bar_target);
         }
@@ -200,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_async_kernel(AsyncParams A) 
         const int len = __shfl_sync(gm, c.y, src);
         float acc = 0.0f;
         if (t > 0) {
-            const float ra = pair0 < len ? ld_l2_f32(A.r + c.x) : 0.0f;
-            const float rb = pair0 + 1 < len ? ld_l2_f32(A.r + c.z) : 0.0f;
+            const float ra = pair0 < len ? ld_l2_f32(A.r + real_row(c.x, A.hot_rows)) : 0.0f;
+            const float rb = pair0 + 1 < len ? ld_l2_f32(A.r + real_row(c.z, A.hot_rows)) : 0.0f;
             acc = fmaf(__int_as_float(c.y), ra, __int_as_float(c.w) * rb);
         }
 #pragma unroll
@@ -217,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_async_kernel(AsyncParams A) 
             }
         }
         d = __shfl_sync(gm, d, src);
-        if (d != 0.0f && t > 0) scatter_chunk(A.r, c, pair0, len, d);
+        if (d != 0.0f && t > 0) scatter_chunk(A.r, c, pair0, len, d, A.hot_rows);
     }
     if (nz) atomicAdd(A.nz_total, nz);
 }
@@ -254,8 +289,20 @@ __global__ void xhdr_out_kernel(const int4* __restrict__ blocks, int G, float* _
 }
 
 // Pack the CSC into blocks: one thread per (column, chunk).
+// row id as stored in a block: 0x80000000 | h if row == hot_rows[h] (ascending list)
+__device__ __forceinline__ int encode_row(int row, const int* __restrict__ hot_rows, int nhot) {
+    int lo = 0, hi = nhot;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (hot_rows[mid] < row) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < nhot && hot_rows[lo] == row) ? (int)(0x80000000u | (unsigned)lo) : row;
+}
+
 __global__ void pack_kernel(int64_t n, int G, const long long* __restrict__ colptr, const int* __restrict__ rowidx,
-                            const float* __restrict__ val, const float* __restrict__ L, int4* __restrict__ blocks) {
+                            const float* __restrict__ val, const float* __restrict__ L, const int* __restrict__ hot_rows,
+                            int nhot, int4* __restrict__ blocks) {
     const int64_t total = n * G;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = q / G;
@@ -267,9 +314,9 @@ __global__ void pack_kernel(int64_t n, int G, const long long* __restrict__ colp
             c = make_int4(__float_as_int(L[i]), len, 0, 0);
         } else {
             const int p0 = 2 * (t - 1);
-            c.x = p0 < len ? rowidx[s + p0] : 0;
+            c.x = p0 < len ? encode_row(rowidx[s + p0], hot_rows, nhot) : 0;
             c.y = p0 < len ? __float_as_int(val[s + p0]) : 0;
-            c.z = p0 + 1 < len ? rowidx[s + p0 + 1] : 0;
+            c.z = p0 + 1 < len ? encode_row(rowidx[s + p0 + 1], hot_rows, nhot) : 0;
             c.w = p0 + 1 < len ? __float_as_int(val[s + p0 + 1]) : 0;
         }
         blocks[q] = c;
@@ -289,7 +336,7 @@ template <int G, bool ONE, bool LOG>
 cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
     void* args[] = {(void*)&P};
     return cudaLaunchCooperativeKernel((const void*)pcdm_packed_kernel<G, ONE, LOG>, dim3(ctas), dim3(kThreads),
-                                       args, 0, st);
+                                       args, packed_smem_bytes(P.nhot), st);
 }
 
 template <bool ONE, bool LOG>
@@ -350,11 +397,13 @@ cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStrea
     return cudaGetLastError();
 }
 
+size_t packed_smem_bytes(int nhot) { return (size_t)nhot * (sizeof(float) + sizeof(int)); }
+
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
-                        int4* blocks, cudaStream_t st, int sms, int64_t* launches) {
+                        const int* hot_rows, int nhot, int4* blocks, cudaStream_t st, int sms, int64_t* launches) {
     int64_t b = (n * G + 255) / 256;
     if (b > sms * 16) b = sms * 16;
-    pack_kernel<<<(int)b, 256, 0, st>>>(n, G, (const long long*)colptr, rowidx, val, L, blocks);
+    pack_kernel<<<(int)b, 256, 0, st>>>(n, G, (const long long*)colptr, rowidx, val, L, hot_rows, nhot, blocks);
     ++*launches;
     return cudaGetLastError();
 }
@@ -387,11 +436,13 @@ cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st,
     return cudaGetLastError();
 }
 
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic) {
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot) {
     int per_sm = 1;
     const void* fn = logistic ? (one_barrier ? kernel_ptr<true, true>(G) : kernel_ptr<false, true>(G))
                               : (one_barrier ? kernel_ptr<true, false>(G) : kernel_ptr<false, false>(G));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess || per_sm < 1)
+    const size_t smem = packed_smem_bytes(nhot);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     return per_sm * sms;
 }

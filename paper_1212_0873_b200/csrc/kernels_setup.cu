@@ -23,6 +23,22 @@ inline int grid_for(int64_t work, int per_block, int max_blocks) {
     return (int)b;
 }
 
+// Hot rows (packed loop, kernels_packed.cu): rows stored >= threshold times are
+// appended (row, count) to a candidate list of capacity cap (n_out counts all).
+__global__ void hot_candidates_kernel(int64_t m, const int* __restrict__ counts, int threshold, int* __restrict__ rows,
+                                      int* __restrict__ cnts, int* __restrict__ n_out, int cap) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+        const int c = counts[j];
+        if (c >= threshold) {
+            const int q = atomicAdd(n_out, 1);
+            if (q < cap) {
+                rows[q] = (int)j;
+                cnts[q] = c;
+            }
+        }
+    }
+}
+
 // One warp per column: colptr monotone, rows in [0,m) and strictly increasing,
 // values finite.
 __global__ void validate_kernel(int64_t m, int64_t n, int64_t nnz, const long long* __restrict__ colptr,
@@ -286,6 +302,16 @@ cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int
     if (e != cudaSuccess) return e;
     const int blocks = grid_for(A.nnz, kThreads, sms * 16);
     row_counts_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, counts);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hot_candidates(int64_t m, const int* counts, int threshold, int* rows, int* cnts, int* n_out,
+                                  int cap, cudaStream_t st, int sms, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(n_out, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    hot_candidates_kernel<<<grid_for(m, kThreads, sms * 8), kThreads, 0, st>>>(m, counts, threshold, rows, cnts, n_out,
+                                                                               cap);
     ++*launches;
     return cudaGetLastError();
 }

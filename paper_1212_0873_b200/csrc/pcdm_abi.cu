@@ -88,6 +88,9 @@ struct pcdm_problem {
     unsigned long long* xlist_count = nullptr;  // |D| (> cap: overflowed, walk all n)
     int64_t xlist_cap = 0;
     int packed_G = 0;          // 0: no packed copy (a column longer than 62 entries)
+    int* hot_rows = nullptr;   // ascending ids of the hot rows cached in shared memory (packed loop)
+    int nhot = 0;
+    int64_t hot_max_count = 0; // stored entries of the most frequent row
     int64_t max_len = 0;
     double* r64 = nullptr;
     float* xbuf = nullptr;     // device iterate when the caller passes host x
@@ -125,6 +128,7 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->r64);
     cudaFree(p->r2);
     cudaFree(p->blocks);
+    cudaFree(p->hot_rows);
     cudaFree(p->xlist);
     cudaFree(p->xlist_count);
     cudaFree(p->xbuf);
@@ -405,6 +409,61 @@ pcdm_status pcdm_create_logistic(int64_t m, int64_t n, int64_t nnz, const int64_
 
 namespace {
 
+// Hot rows of the packed loop (kernels_packed.cu): rows stored at least
+// max(64, 32 x the mean row count) times, the PCDM_HOT_MAX (default 2048) most
+// frequent of them.  Every iteration reads such a row about count_j tau / n times;
+// those same-address reads serialise in one L2 slice unless they are served from
+// the per-CTA shared-memory copy.  Uniform-row configs have none (omega is far
+// below the threshold).  PCDM_HOT_ROWS=0 disables.
+pcdm_status select_hot_rows(pcdm_problem* p, const int* counts, cudaStream_t st, int64_t* launches) {
+    p->nhot = 0;
+    const char* en = getenv("PCDM_HOT_ROWS");
+    if (en && atoi(en) == 0) return PCDM_OK;
+    int hmax = 2048;
+    if (const char* hm = getenv("PCDM_HOT_MAX")) hmax = std::max(0, std::min(8192, atoi(hm)));
+    if (hmax == 0) return PCDM_OK;
+    const int64_t mean = (p->nnz + p->m - 1) / p->m;
+    const int64_t thr64 = std::max<int64_t>(64, 32 * mean);
+    if (thr64 > 0x7fffffff) return PCDM_OK;
+    const int cap = 1 << 16;
+    int *rows = nullptr, *cnts = nullptr, *nout = nullptr;
+    cudaError_t e = cudaMalloc((void**)&rows, sizeof(int) * (2 * cap + 1));
+    if (e != cudaSuccess) return cuda_fail(e, "alloc hot candidates");
+    cnts = rows + cap;
+    nout = rows + 2 * cap;
+    int total = 0;
+    std::vector<int> hr, hc;
+    e = launch_hot_candidates(p->m, counts, (int)thr64, rows, cnts, nout, cap, st, p->sms, launches);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, nout, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    const int got = std::min(total, cap);
+    if (e == cudaSuccess && got > 0) {
+        hr.resize(got);
+        hc.resize(got);
+        e = cudaMemcpyAsync(hr.data(), rows, sizeof(int) * got, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cnts, sizeof(int) * got, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
+    cudaFree(rows);
+    if (e != cudaSuccess) return cuda_fail(e, "hot rows");
+    if (got == 0) return PCDM_OK;
+    // most frequent first (ties: lower row), keep hmax, then ascending row ids
+    std::vector<int> order(got);
+    for (int q = 0; q < got; ++q) order[q] = q;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return hc[a] != hc[b] ? hc[a] > hc[b] : hr[a] < hr[b]; });
+    const int keep = std::min(got, hmax);
+    std::vector<int> sel(keep);
+    for (int q = 0; q < keep; ++q) sel[q] = hr[order[q]];
+    std::sort(sel.begin(), sel.end());
+    e = cudaMalloc((void**)&p->hot_rows, sizeof(int) * keep);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->hot_rows, sel.data(), sizeof(int) * keep, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "hot rows");
+    p->nhot = keep;
+    p->hot_max_count = hc[order[0]];
+    return PCDM_OK;
+}
+
 // loss 0: LASSO with b; loss 1: L2-regularised logistic with labels y (the library
 // stores A~ = diag(y) A, b = 0, L = ||a_i||^2 / 4; R21)
 pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
@@ -458,6 +517,7 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         if (e == cudaSuccess) e = launch_max(m, counts, &p->sc->max_out, st, p->sms, &launches);
         if (e != cudaSuccess) { cudaFree(counts); s = cuda_fail(e, "row histogram"); break; }
         s = read_scalars(p, &hs, st);
+        if (s == PCDM_OK) s = select_hot_rows(p, counts, st, &launches);
         cudaFree(counts);
         if (s != PCDM_OK) break;
         p->omega = hs.max_out;
@@ -470,7 +530,7 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
             const int G = packed_lanes(p->max_len);
             if (cudaMalloc((void**)&p->blocks, (size_t)n * G * 16) == cudaSuccess) {
                 p->packed_G = G;
-                if ((e = launch_pack(n, G, p->colptr, p->rowidx, p->val, p->L, p->blocks, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "pack"); break; }
+                if ((e = launch_pack(n, G, p->colptr, p->rowidx, p->val, p->L, p->hot_rows, p->nhot, p->blocks, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "pack"); break; }
             } else {
                 cudaGetLastError();
                 p->blocks = nullptr;
@@ -598,7 +658,15 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.variant = PCDM_VARIANT_PACKED;
         plan.lanes = p->packed_G;
         plan.threads = 512;
-        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1);
+        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot);
+        // small tau: only CTAs that own slots; the others would only add arrivals to
+        // every grid barrier (PCDM_CTAS overrides, for measurements)
+        const int64_t busy = (tau * p->packed_G + plan.threads - 1) / plan.threads;
+        if (busy < plan.ctas) plan.ctas = (int)busy;
+        if (const char* cs = getenv("PCDM_CTAS")) {
+            const int v = atoi(cs);
+            if (v >= 1) plan.ctas = std::min(v, packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot));
+        }
     }
     if (p->nz_cap < tau) {
         cudaFree(p->nz_idx);
@@ -690,6 +758,14 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.xlist = xhdr ? p->xlist : nullptr;
     Q.xlist_count = p->xlist_count;
     Q.xlist_cap = p->xlist_cap;
+    Q.hot_rows = p->hot_rows;
+    Q.nhot = p->nhot;
+    // cache the hot rows when the hottest one is read >= 1024 times per iteration
+    // (tau count_max / n); below that the per-iteration copy costs more than the
+    // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;
+    // tau = 65536: 548 -> 179 ms/step of iteration kernel, profiles/r01_hot_rows_ab.jsonl)
+    Q.hot_cache = p->nhot > 0 && (double)tau * (double)p->hot_max_count >= 1024.0 * (double)p->n;
+    if (const char* hc = getenv("PCDM_HOT_CACHE")) Q.hot_cache = p->nhot > 0 && atoi(hc) != 0;
 
     int64_t done = 0;
     while (done < iters) {
@@ -751,6 +827,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     stats.threads_per_cta = plan.threads;
     stats.lanes_per_column = plan.lanes;
     stats.chunk_iters = chunk;
+    stats.hot_rows = packed && Q.hot_cache ? p->nhot : 0;
     double tms[3];
     tm.sum(tms);
     stats.iter_kernel_ms = tms[T_ITER];
@@ -813,6 +890,7 @@ pcdm_status pcdm_run_async(pcdm_problem* p, float* x, int64_t updates, int64_t t
     A.lambda = (float)p->lambda;
     A.flags = &p->sc->flags;
     A.nz_total = &p->sc->nz_total;
+    A.hot_rows = p->hot_rows;
     for (int64_t done = 0; done < updates;) {
         const int64_t c = R > 0 ? std::min(R, updates - done) : updates - done;
         A.updates = c;
