@@ -76,6 +76,25 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& target
     __syncthreads();
 }
 
+// Split form: work issued between arrive and wait overlaps the other CTAs' arrival
+// (it must not write anything the barrier is meant to publish).
+__device__ __forceinline__ void grid_arrive(unsigned* counter, unsigned& target) {
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+    }
+}
+__device__ __forceinline__ void grid_wait(const unsigned* counter, unsigned target) {
+    if (threadIdx.x == 0) {
+        while ((int)(ld_acquire_u32(counter) - target) < 0) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------- Philox4x32-10
 struct u32x4 { uint32_t x, y, z, w; };
 

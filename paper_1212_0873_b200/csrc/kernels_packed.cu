@@ -23,7 +23,10 @@
 //                Q = r_{k-1}: iteration k gathers from P and scatters both its
 //                own steps Delta_k and the previous iteration's list Delta_{k-1}
 //                into Q, so after ONE barrier Q = r_{k-1} + Delta_{k-1} + Delta_k
-//                = r_{k+1} and the buffers swap.  Used when 2 r fits in L2.
+//                = r_{k+1} and the buffers swap (the default).  The replay of
+//                Delta_{k-1} is issued at the start of iteration k, so its dependent
+//                loads overlap the gathers; the first slot of iteration k+1 (S and its
+//                block do not depend on r) is loaded between barrier arrival and wait.
 // Step lists rotate over 3 buffers (append k%3, replay (k-1)%3, reset (k+1)%3).
 //
 // Hot rows (skewed row distributions, e.g. the Zipf config): a row stored in a
@@ -110,6 +113,19 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
         __syncthreads();
     }
 
+    // software pipeline: slot gid of iteration it and its block, loaded one iteration ahead
+    int i_pf = -1;
+    int4 c_pf = make_int4(0, 0, 0, 0);
+    auto prefetch = [&](int64_t it) {
+        i_pf = -1;
+        if (it < P.iters && gid < tau) {
+            i_pf = ld_stream_s32(P.slots + it * tau + gid);
+            if (i_pf >= 0)
+                c_pf = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i_pf * G + t) : ld_stream_v4(P.blocks + (int64_t)i_pf * G + t);
+        }
+    };
+    prefetch(0);
+
     for (int64_t it = 0; it < P.iters; ++it) {
         const int64_t k = P.k0 + it;
         const int cur = (int)(k % 3), prev = (int)((k + 2) % 3), next = (int)((k + 1) % 3);
@@ -117,6 +133,18 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
         float* rQ = (ONE_BARRIER && (k & 1)) ? P.r0 : P.r1;
         const int* S = P.slots + it * tau;
         if (blockIdx.x == 0 && threadIdx.x == 0) P.nz_count[next] = 0;
+        if (ONE_BARRIER) {
+            // replay the previous iteration's nonzero steps into Q (first, so that its
+            // dependent loads overlap phase A instead of following it)
+            const int cntp = ld_l2_s32(P.nz_count + prev);
+            for (int64_t e = gid; e < cntp; e += ngroups) {
+                const int i = ld_l2_s32(P.nz_idx + prev * tau + e);
+                const float d = ld_l2_f32(P.nz_delta + prev * tau + e);
+                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int len = __shfl_sync(gm, c.y, src);
+                if (t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+            }
+        }
         if (cache && has_slots) {
             // the previous iteration's readers of s_hot passed the grid barrier's __syncthreads
             for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hot[h] = ld_l2_f32(rP + s_hrow[h]);
@@ -125,14 +153,26 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
 
         // ---------------- phase A: one coalesced block load + <= 2 gathers per lane
         for (int64_t j = gid; j < tau; j += ngroups) {
-            const int i = ld_stream_s32(S + j);
-            if (i < 0) continue;  // idle processor (non-nice samplings)
+            int i;
+            int4 c;
             float xi = 0.0f;
-            // x_i lives in the block header (chunk 0 .z) when P.xlist: the column's single
-            // line brings it, no separate random x line; the header is then mutable, so
-            // the block is read through L2 (ld.cg) instead of the non-coherent path
-            const int4 c = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i * G + t) : ld_stream_v4(P.blocks + (int64_t)i * G + t);
-            if (t == 0) xi = P.xlist ? __int_as_float(c.z) : ld_l2_f32(P.x + i);
+            if (j == gid) {
+                // this group's first slot was loaded before the previous barrier (S_k and
+                // the block do not depend on r); only x_i, which a step of iteration k-1
+                // may have changed, is read again
+                i = i_pf;
+                c = c_pf;
+                if (i < 0) continue;
+                if (t == 0) xi = P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : ld_l2_f32(P.x + i);
+            } else {
+                i = ld_stream_s32(S + j);
+                if (i < 0) continue;  // idle processor (non-nice samplings)
+                // x_i lives in the block header (chunk 0 .z) when P.xlist: the column's single
+                // line brings it, no separate random x line; the header is then mutable, so
+                // the block is read through L2 (ld.cg) instead of the non-coherent path
+                c = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i * G + t) : ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                if (t == 0) xi = P.xlist ? __int_as_float(c.z) : ld_l2_f32(P.x + i);
+            }
             const int len = __shfl_sync(gm, c.y, src);
             float acc = 0.0f;
             if (t > 0) {
@@ -166,16 +206,10 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
             }
         }
         if (ONE_BARRIER) {
-            // replay the previous iteration's nonzero steps into Q
-            const int cntp = ld_l2_s32(P.nz_count + prev);
-            for (int64_t e = gid; e < cntp; e += ngroups) {
-                const int i = ld_l2_s32(P.nz_idx + prev * tau + e);
-                const float d = ld_l2_f32(P.nz_delta + prev * tau + e);
-                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
-                const int len = __shfl_sync(gm, c.y, src);
-                if (t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
-            }
-            grid_barrier(P.barrier, bar_target);
+            // the next iteration's first slot is loaded while the other CTAs arrive
+            grid_arrive(P.barrier, bar_target);
+            prefetch(it + 1);
+            grid_wait(P.barrier, bar_target);
         } else {
             grid_barrier(P.barrier, bar_target);
             const int cnt = ld_l2_s32(P.nz_count + cur);
@@ -186,7 +220,9 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
                 const int len = __shfl_sync(gm, c.y, src);
                 if (t > 0) scatter_chunk(P.r0, c, pair0, len, d, s_hrow);
             }
-            grid_barrier(P.barrier, bar_target);
+            grid_arrive(P.barrier, bar_target);
+            prefetch(it + 1);
+            grid_wait(P.barrier, bar_target);
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             const int cnt = ld_l2_s32(P.nz_count + cur);
