@@ -62,9 +62,16 @@ typedef enum {
     PCDM_VARIANT_GRID = 1, /* persistent cooperative grid, r in HBM/L2, grid barriers    */
     PCDM_VARIANT_SMEM = 2, /* one CTA, A, r, x, L resident in shared memory (small A)    */
     PCDM_VARIANT_BLOCK = 3, /* one CTA, data in HBM/L2, __syncthreads barriers           */
-    PCDM_VARIANT_PACKED = 4 /* persistent grid on packed column blocks (one coalesced line
+    PCDM_VARIANT_PACKED = 4, /* persistent grid on packed column blocks (one coalesced line
                                per column); one barrier per iteration with double-buffered
-                               r when 2r fits in L2, else two.  Needs max column length <= 62 */
+                               r (PCDM_ONE_BARRIER=0: two).  Needs max column length <= 62 */
+    PCDM_VARIANT_BATCHED = 5 /* packed blocks; per chunk of iterations the partial
+                               derivatives a_i^T r_0 of all sampled columns are computed at
+                               once from the chunk's starting residual (gathers sorted by
+                               row bin, r streamed through L2 once per chunk), plus
+                               a_i^T (r_k - r_0) on the rows the chunk's steps touched.
+                               Same iteration (alg:PCD1), different summation order of g_i.
+                               For r much larger than L2.  Needs max column length <= 62 */
 } pcdm_variant;
 
 /* Doubly uniform samplings (tbl:ESO PAPER.md:324-355).  A run

@@ -167,6 +167,43 @@ cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams&
                           int64_t* launches);
 size_t packed_smem_bytes(int nhot);
 
+// ---- batched-snapshot loop (kernels_batched.cu): passes expand / sweep / steps / fold
+struct BatchedParams {
+    int4* blocks;         // packed column blocks (as PackedParams)
+    const int* slots;     // [iters][tau] of the chunk
+    int64_t tau;
+    int64_t iters;        // iterations of the chunk (c)
+    float beta;
+    float lambda;
+    const float* r;       // residual (margins) r_0 at the start of the chunk, read-only in passes 1-3
+    float* r_out;         // the same buffer, updated by the fold
+    float* d0;            // D = r_k - r_0 double buffer, zero outside the chunk's dirty rows
+    float* d1;
+    float* g0;            // [iters * tau] a_i^T w(r_0) per chunk slot
+    int2* gent;           // [nq][cq * maxe] sorted entries (row_local | slot_local << rb, val)
+    int* offs;            // [nq][nb + 1] bin starts
+    int nq, cq_log, nb, rb, maxe;
+    int2* rec;            // [iters * tau][G] slot records: lane 0 {L_i, x_i}, lane t real rows 2t-2, 2t-1 (-1: none)
+    int* nz_idx;          // [iters][tau] nonzero steps per iteration
+    float* nz_delta;      // [iters][tau]
+    int* nz_count;        // [iters], zeroed before the chunk
+    unsigned* barrier;
+    int* flags;
+    unsigned long long* nz_total;
+    float* x;
+    int* xlist;
+    unsigned long long* xlist_count;
+    int64_t xlist_cap;
+    const int* hot_rows;
+    int nhot;
+    int logistic;
+};
+size_t batched_step_smem(int nhot);
+int batched_cq_log(int G);
+int batched_rb(int cq_log);
+int batched_ctas(int G, int sms, bool logistic, int nhot);
+cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches);
+
 // Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
 IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,
                      bool logistic = false);

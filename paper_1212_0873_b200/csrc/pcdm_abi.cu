@@ -91,6 +91,10 @@ struct pcdm_problem {
     int* hot_rows = nullptr;   // ascending ids of the hot rows cached in shared memory (packed loop)
     int nhot = 0;
     int64_t hot_max_count = 0; // stored entries of the most frequent row
+    float* d0 = nullptr;       // BATCHED: D = r_k - r_0 double buffer (zero between chunks)
+    float* d1 = nullptr;
+    void* bat_mem = nullptr;   // BATCHED per-chunk workspace (g0, sorted entries, offsets, lists)
+    size_t bat_cap = 0;
     int64_t max_len = 0;
     double* r64 = nullptr;
     float* xbuf = nullptr;     // device iterate when the caller passes host x
@@ -129,6 +133,9 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->r2);
     cudaFree(p->blocks);
     cudaFree(p->hot_rows);
+    cudaFree(p->d0);
+    cudaFree(p->d1);
+    cudaFree(p->bat_mem);
     cudaFree(p->xlist);
     cudaFree(p->xlist_count);
     cudaFree(p->xbuf);
@@ -609,8 +616,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const int64_t tau = spec.tau;
     if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
     if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
-    if (variant < 0 || variant > 4) return fail(PCDM_EINVAL, "unknown variant %d", variant);
-    if (variant == PCDM_VARIANT_PACKED && !p->packed_G)
+    if (variant < 0 || variant > 5) return fail(PCDM_EINVAL, "unknown variant %d", variant);
+    if ((variant == PCDM_VARIANT_PACKED || variant == PCDM_VARIANT_BATCHED) && !p->packed_G)
         return fail(PCDM_EINVAL, "PACKED variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
@@ -636,11 +643,15 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     double beta_d = sampling_beta(spec, p->omega, p->n);
     if (beta_override > 0.0) beta_d = beta_override;
     const int64_t R = refresh_period(p->n, tau, refresh_every);
-    IterLaunch plan = plan_iter(variant == PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
+    IterLaunch plan = plan_iter(variant >= PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
                                 p->sms, p->device, p->loss == 1);
     // AUTO: packed blocks whenever the shared-memory variant does not apply
-    const bool packed = p->packed_G > 0 &&
-                        (variant == PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
+    bool packed = p->packed_G > 0 &&
+                  (variant >= PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
+    // BATCHED (kernels_batched.cu): on request only, for now
+    bool batched = packed && (variant == PCDM_VARIANT_BATCHED ||
+                              (variant == PCDM_VARIANT_AUTO && getenv("PCDM_BATCHED") && atoi(getenv("PCDM_BATCHED")) != 0));
+    if (batched) packed = false;
     bool one_barrier = false;
     if (packed) {
         // one barrier per iteration (double-buffered r, the previous iteration's steps
@@ -682,7 +693,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // update; PCDM_X_IN_BLOCK=0 keeps x in the caller's array.  The start-of-run
     // header load rides on the residual pass, which reads x anyway.
     const char* xib = getenv("PCDM_X_IN_BLOCK");
-    const bool xhdr = packed && !(xib && atoi(xib) == 0);
+    const bool xhdr = (packed || batched) && !(xib && atoi(xib) == 0);
     XHeaders xh{};
     if (xhdr) {
         if (!p->xlist) {
@@ -767,6 +778,71 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.hot_cache = p->nhot > 0 && (double)tau * (double)p->hot_max_count >= 1024.0 * (double)p->n;
     if (const char* hc = getenv("PCDM_HOT_CACHE")) Q.hot_cache = p->nhot > 0 && atoi(hc) != 0;
 
+    BatchedParams B{};
+    int bat_ctas = 0;
+    if (batched) {
+        const int G = p->packed_G;
+        B.cq_log = batched_cq_log(G);
+        B.rb = batched_rb(B.cq_log);
+        B.maxe = 2 * (G - 1);
+        B.nb = (int)((p->m + (1ll << B.rb) - 1) >> B.rb);
+        const int64_t cq = 1ll << B.cq_log;
+        const int64_t nq_max = (chunk * tau + cq - 1) / cq;
+        auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+        const size_t o_g0 = 0;
+        const size_t o_ent = o_g0 + al(sizeof(float) * chunk * tau);
+        const size_t o_offs = o_ent + al(sizeof(int2) * nq_max * cq * B.maxe);
+        const size_t o_idx = o_offs + al(sizeof(int) * nq_max * (B.nb + 1));
+        const size_t o_del = o_idx + al(sizeof(int) * chunk * tau);
+        const size_t o_cnt = o_del + al(sizeof(float) * chunk * tau);
+        const size_t o_rec = o_cnt + al(sizeof(int) * chunk);
+        const size_t need = o_rec + al(sizeof(int2) * chunk * tau * G);
+        if (p->bat_cap < need) {
+            cudaFree(p->bat_mem);
+            p->bat_mem = nullptr;
+            p->bat_cap = 0;
+            CK(cudaMalloc(&p->bat_mem, need), "alloc batched workspace");
+            p->bat_cap = need;
+        }
+        if (!p->d0) {
+            CK(cudaMalloc((void**)&p->d0, sizeof(float) * p->m), "alloc delta buffer");
+            CK(cudaMalloc((void**)&p->d1, sizeof(float) * p->m), "alloc delta buffer");
+            CK(cudaMemsetAsync(p->d0, 0, sizeof(float) * p->m, st), "memset delta");
+            CK(cudaMemsetAsync(p->d1, 0, sizeof(float) * p->m, st), "memset delta");
+        }
+        char* base = (char*)p->bat_mem;
+        B.blocks = p->blocks;
+        B.tau = tau;
+        B.beta = (float)beta_d;
+        B.lambda = (float)p->lambda;
+        B.r = p->r;
+        B.r_out = p->r;
+        B.d0 = p->d0;
+        B.d1 = p->d1;
+        B.g0 = (float*)(base + o_g0);
+        B.gent = (int2*)(base + o_ent);
+        B.offs = (int*)(base + o_offs);
+        B.nz_idx = (int*)(base + o_idx);
+        B.nz_delta = (float*)(base + o_del);
+        B.nz_count = (int*)(base + o_cnt);
+        B.rec = (int2*)(base + o_rec);
+        B.barrier = &p->sc->barrier;
+        B.flags = &p->sc->flags;
+        B.nz_total = &p->sc->nz_total;
+        B.x = xd;
+        B.xlist = xhdr ? p->xlist : nullptr;
+        B.xlist_count = p->xlist_count;
+        B.xlist_cap = p->xlist_cap;
+        B.hot_rows = p->hot_rows;
+        B.nhot = p->nhot;
+        B.logistic = p->loss;
+        bat_ctas = batched_ctas(G, p->sms, p->loss == 1, p->nhot);
+        plan.variant = PCDM_VARIANT_BATCHED;
+        plan.lanes = G;
+        plan.threads = 512;
+        plan.ctas = bat_ctas;
+    }
+
     int64_t done = 0;
     while (done < iters) {
         int64_t c = std::min(chunk, iters - done);
@@ -777,12 +853,18 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
            "sampler");
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
-        CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed ? 0 : 3 * sizeof(int)), st),
+        CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed || batched ? 0 : 3 * sizeof(int)), st),
            "memset barrier");
+        if (batched) CK(cudaMemsetAsync(B.nz_count, 0, sizeof(int) * c, st), "memset step lists");
         CK(tm.end(T_SAMPLER, ts), "event");
         int ti;
         CK(tm.begin(&ti), "event");
-        if (packed) {
+        if (batched) {
+            B.slots = sp.slots;
+            B.iters = c;
+            B.nq = (int)((c * tau + (1ll << B.cq_log) - 1) >> B.cq_log);
+            CK(launch_batched(p->packed_G, B, bat_ctas, st, p->sms, &launches), "batched iteration kernels");
+        } else if (packed) {
             Q.slots = sp.slots;
             Q.iters = c;
             Q.k0 = done;
