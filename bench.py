@@ -39,9 +39,10 @@ from paper_1212_0873_b200 import instances as I  # noqa: E402
 
 METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline) at 1 B200"
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
-VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", -1: "async"}
+VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", 6: "cluster", -1: "async"}
 KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
-                     5: "batch_expand+batch_sweep+pcdm_batched+batch_fold", -1: "pcdm_async_kernel"}
+                     5: "batch_expand+batch_sweep+pcdm_batched+batch_fold", 6: "pcdm_cluster_kernel",
+                     -1: "pcdm_async_kernel"}
 # oracle iterations per reference step / cpu_baseline sample, per config
 REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4, "logistic_small": 200, "kddb_like": 4}
 CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24, "logistic_small": 1000,

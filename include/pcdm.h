@@ -65,13 +65,20 @@ typedef enum {
     PCDM_VARIANT_PACKED = 4, /* persistent grid on packed column blocks (one coalesced line
                                per column); one barrier per iteration with double-buffered
                                r (PCDM_ONE_BARRIER=0: two).  Needs max column length <= 62 */
-    PCDM_VARIANT_BATCHED = 5 /* packed blocks; per chunk of iterations the partial
+    PCDM_VARIANT_BATCHED = 5, /* packed blocks; per chunk of iterations the partial
                                derivatives a_i^T r_0 of all sampled columns are computed at
                                once from the chunk's starting residual (gathers sorted by
                                row bin, r streamed through L2 once per chunk), plus
                                a_i^T (r_k - r_0) on the rows the chunk's steps touched.
                                Same iteration (alg:PCD1), different summation order of g_i.
                                For r much larger than L2.  Needs max column length <= 62 */
+    PCDM_VARIANT_CLUSTER = 6 /* packed blocks; r split over the shared memories of one
+                               thread-block cluster (<= 16 CTAs), gathers and scatters in
+                               distributed shared memory, two hardware cluster barriers per
+                               iteration.  Needs 4m bytes / cluster size to fit in shared
+                               memory (m <= ~900K) and max column length <= 62.  Measured
+                               slower than PACKED on medium; AUTO picks it only with
+                               PCDM_CLUSTER=1 */
 } pcdm_variant;
 
 /* Doubly uniform samplings (tbl:ESO PAPER.md:324-355).  A run

@@ -616,8 +616,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const int64_t tau = spec.tau;
     if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
     if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
-    if (variant < 0 || variant > 5) return fail(PCDM_EINVAL, "unknown variant %d", variant);
-    if ((variant == PCDM_VARIANT_PACKED || variant == PCDM_VARIANT_BATCHED) && !p->packed_G)
+    if (variant < 0 || variant > 6) return fail(PCDM_EINVAL, "unknown variant %d", variant);
+    if ((variant == PCDM_VARIANT_PACKED || variant == PCDM_VARIANT_BATCHED || variant == PCDM_VARIANT_CLUSTER) &&
+        !p->packed_G)
         return fail(PCDM_EINVAL, "PACKED variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
@@ -652,6 +653,36 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     bool batched = packed && (variant == PCDM_VARIANT_BATCHED ||
                               (variant == PCDM_VARIANT_AUTO && getenv("PCDM_BATCHED") && atoi(getenv("PCDM_BATCHED")) != 0));
     if (batched) packed = false;
+    // CLUSTER (kernels_cluster.cu): r in one cluster's distributed shared memory
+    int cl_size = 0, cl_rpc = 0, cl_cap = 0;
+    size_t cl_smem = 0;
+    if (packed && (variant == PCDM_VARIANT_CLUSTER || variant == PCDM_VARIANT_AUTO)) {
+        // AUTO only with PCDM_CLUSTER=1: measured slower than the grid loop on medium
+        // (5.0 vs 3.8 us per iteration, profiles/r01_cluster_medium_ab.jsonl)
+        const char* ce = getenv("PCDM_CLUSTER");
+        const bool allow = variant == PCDM_VARIANT_CLUSTER || (ce && atoi(ce) != 0);
+        // AUTO: only when every group has at most two slots per iteration on 16 CTAs
+        const bool small_tau = variant == PCDM_VARIANT_CLUSTER || tau * p->packed_G <= 2 * 16 * 1024;
+        for (int want = 16; allow && small_tau && want >= 2 && !cl_size; want >>= 1) {
+            const int64_t rpc = ((p->m + want - 1) / want + 3) & ~(int64_t)3;  // keeps the step list 8-byte aligned
+            const int64_t groups = (int64_t)want * 1024 / p->packed_G;
+            const int64_t cap = ((tau + groups - 1) / groups) * (1024 / p->packed_G);
+            const size_t smem = cluster_smem_bytes((int)std::min<int64_t>(rpc, 1 << 28), p->nhot, (int)cap);
+            if (smem > 220 * 1024) continue;
+            const int cs = cluster_plan(p->packed_G, p->loss == 1, smem, want);
+            if (cs == want) {
+                cl_size = cs;
+                cl_rpc = (int)rpc;
+                cl_cap = (int)cap;
+                cl_smem = smem;
+            }
+        }
+        if (variant == PCDM_VARIANT_CLUSTER && !cl_size)
+            return fail(PCDM_EINVAL, "CLUSTER variant: r (m = %lld) does not fit in one cluster's shared memory",
+                        (long long)p->m);
+    }
+    const bool clustered = cl_size > 0;
+    if (clustered) packed = false;
     bool one_barrier = false;
     if (packed) {
         // one barrier per iteration (double-buffered r, the previous iteration's steps
@@ -693,7 +724,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // update; PCDM_X_IN_BLOCK=0 keeps x in the caller's array.  The start-of-run
     // header load rides on the residual pass, which reads x anyway.
     const char* xib = getenv("PCDM_X_IN_BLOCK");
-    const bool xhdr = (packed || batched) && !(xib && atoi(xib) == 0);
+    const bool xhdr = (packed || batched || clustered) && !(xib && atoi(xib) == 0);
     XHeaders xh{};
     if (xhdr) {
         if (!p->xlist) {
@@ -843,6 +874,31 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.ctas = bat_ctas;
     }
 
+    ClusterParams CP{};
+    if (clustered) {
+        CP.blocks = p->blocks;
+        CP.tau = tau;
+        CP.beta = (float)beta_d;
+        CP.lambda = (float)p->lambda;
+        CP.r = p->r;
+        CP.m = p->m;
+        CP.rpc = cl_rpc;
+        CP.x = xd;
+        CP.xlist = xhdr ? p->xlist : nullptr;
+        CP.xlist_count = p->xlist_count;
+        CP.xlist_cap = p->xlist_cap;
+        CP.hot_rows = p->hot_rows;
+        CP.nhot = p->nhot;
+        CP.list_cap = cl_cap;
+        CP.flags = &p->sc->flags;
+        CP.nz_total = &p->sc->nz_total;
+        CP.logistic = p->loss;
+        plan.variant = PCDM_VARIANT_CLUSTER;
+        plan.lanes = p->packed_G;
+        plan.threads = 1024;
+        plan.ctas = cl_size;
+    }
+
     int64_t done = 0;
     while (done < iters) {
         int64_t c = std::min(chunk, iters - done);
@@ -859,7 +915,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(tm.end(T_SAMPLER, ts), "event");
         int ti;
         CK(tm.begin(&ti), "event");
-        if (batched) {
+        if (clustered) {
+            CP.slots = sp.slots;
+            CP.iters = c;
+            CK(launch_cluster(p->packed_G, cl_size, CP, cl_smem, st, &launches), "cluster iteration kernel");
+        } else if (batched) {
             B.slots = sp.slots;
             B.iters = c;
             B.nq = (int)((c * tau + (1ll << B.cq_log) - 1) >> B.cq_log);

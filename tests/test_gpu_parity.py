@@ -109,7 +109,8 @@ def test_tiny_config_full_run(gpu, variant):
 
 def test_medium_config_full_run(gpu):
     inst = I.generate("medium", seed=0)
-    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 1024, 10_000, seed=0)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 1024, 10_000, seed=0,
+                   variant="packed")
     assert_parity(out)
     assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
 
