@@ -132,6 +132,10 @@ typedef struct {
                                    copy of r (rows stored >= max(64, 32 x mean) times,
                                    the 2048 most frequent; 0 for uniform rows, and 0
                                    when tau x (count of the hottest row) < 1024 n)    */
+    int64_t host_h2d_bytes;     /* host x: bytes copied host -> device by the run      */
+    int64_t host_d2h_bytes;     /* host x: bytes copied device -> host (the changed
+                                   entries only, as (index, value) pairs, when they are
+                                   fewer than n/2; else the whole x)                  */
 } pcdm_run_stats;
 
 /* pcdm_create -- build a problem handle for LASSO with A (m x n, CSC), b, lambda.

@@ -158,6 +158,8 @@ struct AsyncParams {
 int async_groups(int G, int sms, int* ctas);
 cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st, int64_t* launches);
 int packed_lanes(int64_t max_len);
+cudaError_t launch_gather_list(const float* x, const int* list, int64_t count, float* out, cudaStream_t st, int sms,
+                               int64_t* launches);
 cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStream_t st, int sms, int64_t* launches);
 // rows listed in hot_rows[0..nhot) (ascending) are stored as 0x80000000 | h
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,

@@ -324,6 +324,13 @@ __global__ void xhdr_out_kernel(const int4* __restrict__ blocks, int G, float* _
     }
 }
 
+// out[t] = x[list[t]], t < count (the changed entries of a host iterate, copied back compactly)
+__global__ void gather_list_kernel(const float* __restrict__ x, const int* __restrict__ list, int64_t count,
+                                   float* __restrict__ out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = x[list[t]];
+}
+
 // Pack the CSC into blocks: one thread per (column, chunk).
 // row id as stored in a block: 0x80000000 | h if row == hot_rows[h] (ascending list)
 __device__ __forceinline__ int encode_row(int row, const int* __restrict__ hot_rows, int nhot) {
@@ -429,6 +436,16 @@ cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStrea
     int64_t b = (n + 255) / 256;
     if (b > sms * 8) b = sms * 8;
     max_len_kernel<<<(int)b, 256, 0, st>>>(n, (const long long*)colptr, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_list(const float* x, const int* list, int64_t count, float* out, cudaStream_t st, int sms,
+                               int64_t* launches) {
+    int64_t b = (count + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > sms * 8) b = sms * 8;
+    gather_list_kernel<<<(int)b, 256, 0, st>>>(x, list, count, out);
     ++*launches;
     return cudaGetLastError();
 }

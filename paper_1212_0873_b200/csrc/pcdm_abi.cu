@@ -98,6 +98,10 @@ struct pcdm_problem {
     int64_t max_len = 0;
     double* r64 = nullptr;
     float* xbuf = nullptr;     // device iterate when the caller passes host x
+    float* xcomp = nullptr;    // changed entries of xbuf, gathered for the compact copy back
+    int* hidx = nullptr;       // pinned host staging of the compact copy (indices, values)
+    float* hval = nullptr;
+    int64_t comp_cap = 0;
     Scalars* sc = nullptr;     // device scalars
     // per-run workspaces (grown on demand)
     int* nz_idx = nullptr;
@@ -139,6 +143,9 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->xlist);
     cudaFree(p->xlist_count);
     cudaFree(p->xbuf);
+    cudaFree(p->xcomp);
+    cudaFreeHost(p->hidx);
+    cudaFreeHost(p->hval);
     cudaFree(p->sc);
     cudaFree(p->nz_idx);
     cudaFree(p->nz_delta);
@@ -954,7 +961,45 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     int tx;
     CK(tm.begin(&tx), "event");
     if ((s = x_out()) != PCDM_OK) return s;
-    if (!x_dev) CK(cudaMemcpyAsync(x, p->xbuf, sizeof(float) * p->n, cudaMemcpyDeviceToHost, st), "copy x out");
+    if (!x_dev) {
+        stats.host_h2d_bytes = (int64_t)sizeof(float) * p->n;
+        // with x in the block headers the dirty list names every entry the run may have
+        // changed: copy back (index, value) pairs when that is less than the whole x
+        bool compact = false;
+        unsigned long long cnt = 0;
+        if (xhdr) {
+            CK(cudaMemcpyAsync(&cnt, p->xlist_count, sizeof(cnt), cudaMemcpyDeviceToHost, st), "read x list");
+            CK(cudaStreamSynchronize(st), "stream synchronize");
+            compact = cnt <= (unsigned long long)p->xlist_cap && 8 * (int64_t)cnt < 4 * p->n;
+        }
+        if (compact && cnt > 0) {
+            if (p->comp_cap < (int64_t)cnt) {
+                cudaFree(p->xcomp);
+                cudaFreeHost(p->hidx);
+                cudaFreeHost(p->hval);
+                p->xcomp = nullptr;
+                p->hidx = nullptr;
+                p->hval = nullptr;
+                p->comp_cap = 0;
+                const int64_t cap = std::max<int64_t>((int64_t)cnt, 1 << 16);
+                CK(cudaMalloc((void**)&p->xcomp, sizeof(float) * cap), "alloc compact x");
+                CK(cudaMallocHost((void**)&p->hidx, sizeof(int) * cap), "alloc compact x");
+                CK(cudaMallocHost((void**)&p->hval, sizeof(float) * cap), "alloc compact x");
+                p->comp_cap = cap;
+            }
+            CK(launch_gather_list(p->xbuf, p->xlist, (int64_t)cnt, p->xcomp, st, p->sms, &launches), "gather x");
+            CK(cudaMemcpyAsync(p->hidx, p->xlist, sizeof(int) * cnt, cudaMemcpyDeviceToHost, st), "copy x out");
+            CK(cudaMemcpyAsync(p->hval, p->xcomp, sizeof(float) * cnt, cudaMemcpyDeviceToHost, st), "copy x out");
+            CK(cudaStreamSynchronize(st), "stream synchronize");
+            for (unsigned long long q = 0; q < cnt; ++q) x[p->hidx[q]] = p->hval[q];
+            stats.host_d2h_bytes = (int64_t)sizeof(cnt) + 8 * (int64_t)cnt;
+        } else if (!compact) {
+            CK(cudaMemcpyAsync(x, p->xbuf, sizeof(float) * p->n, cudaMemcpyDeviceToHost, st), "copy x out");
+            stats.host_d2h_bytes = (int64_t)sizeof(float) * p->n;
+        } else {
+            stats.host_d2h_bytes = (int64_t)sizeof(cnt);
+        }
+    }
     CK(tm.end(T_SETUP, tx), "event");
     int rmax = 0;
     CK(cudaMemcpyAsync(&rmax, sp.w.rounds_max, sizeof(int), cudaMemcpyDeviceToHost, st), "read rounds");

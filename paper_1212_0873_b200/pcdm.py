@@ -43,7 +43,8 @@ class RunStats(ctypes.Structure):
                 ("lanes_per_column", ctypes.c_int32), ("chunk_iters", ctypes.c_int64),
                 ("iter_launches", ctypes.c_int64), ("iter_kernel_ms", ctypes.c_double),
                 ("sampler_ms", ctypes.c_double), ("setup_ms", ctypes.c_double),
-                ("hot_rows", ctypes.c_int64)]
+                ("hot_rows", ctypes.c_int64), ("host_h2d_bytes", ctypes.c_int64),
+                ("host_d2h_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -372,3 +372,31 @@ def test_caller_changes_x_between_runs(gpu):
     xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), lam, 128, 50, 3).x
     assert np.max(np.abs(to_host(x) - xo)) <= 1e-4 * np.max(np.abs(xo))
     prob.close()
+
+
+# ------------------------------------------------------------------ host x: compact copy-back
+@pytest.mark.parametrize("cap", [None, "3"], ids=["compact", "list-overflow"])
+def test_host_x_compact_copy_back(gpu, monkeypatch, cap):
+    # packed loop with x in the block headers: only the dirty entries travel back to the host
+    if cap:
+        monkeypatch.setenv("PCDM_XLIST_CAP", cap)
+    m, n = 6000, 20_000
+    c, r, v, b, lam = _ragged(m, n, np.full(n, 8), 51, lam_frac=0.3)
+    x0 = np.zeros(n, dtype=np.float32)
+    x0[::997] = np.random.default_rng(7).normal(size=x0[::997].size).astype(np.float32)
+    prob = pcdm.Problem(m, n, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), lam)
+    xh = x0.copy()
+    xd = torch.from_numpy(x0.copy()).to(gpu)
+    prob.run(xh, 256, 40, seed=9, variant="packed")
+    st = prob.stats()
+    prob.run(xd, 256, 40, seed=9, variant="packed")
+    np.testing.assert_allclose(xh, to_host(xd), rtol=1e-5, atol=1e-6)
+    assert st["host_h2d_bytes"] == 4 * n
+    if cap:
+        assert st["host_d2h_bytes"] == 4 * n
+    else:
+        assert 0 < st["host_d2h_bytes"] < 4 * n // 4
+    xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), lam, 256, 40, 9,
+                    x0=x0.astype(np.float64)).x
+    assert np.max(np.abs(xh - xo)) <= 1e-4 * np.max(np.abs(xo))
+    prob.close()
