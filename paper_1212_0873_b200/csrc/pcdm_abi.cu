@@ -102,6 +102,10 @@ struct pcdm_problem {
     int* hidx = nullptr;       // pinned host staging of the compact copy (indices, values)
     float* hval = nullptr;
     int64_t comp_cap = 0;
+    int* pre_slots = nullptr;  // host-x runs: the whole run's slot arrays, drawn during the x copy
+    size_t pre_cap = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
     Scalars* sc = nullptr;     // device scalars
     // per-run workspaces (grown on demand)
     int* nz_idx = nullptr;
@@ -146,6 +150,13 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->xcomp);
     cudaFreeHost(p->hidx);
     cudaFreeHost(p->hval);
+    cudaFree(p->pre_slots);
+    if (p->side) {
+        cudaStreamDestroy(p->side);
+        cudaEventDestroy(p->ev_fork);
+        cudaEventDestroy(p->ev_s0);
+        cudaEventDestroy(p->ev_s1);
+    }
     cudaFree(p->sc);
     cudaFree(p->nz_idx);
     cudaFree(p->nz_delta);
@@ -636,21 +647,72 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     RunTimer tm{p, st};
     int t0;
     CK(tm.begin(&t0), "event");
+    // a previous host-x run's side-stream sampler must be done with the workspace
+    if (p->side) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
     // iterate buffer: device x in place, host x through xbuf
     const bool x_dev = is_device_ptr(x);
+    CK(cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st), "memset scalars");
+    pcdm_status s = PCDM_OK;
+    Scalars hs{};
+    // sampler plan: chunks of iterations, aligned with the residual refreshes
+    const int64_t R = refresh_period(p->n, tau, refresh_every);
+    int64_t chunk = choose_chunk(p->n, tau, iters);
+    if (R > 0) chunk = std::min(chunk, R);
+    auto chunk_len = [&](int64_t done) {
+        int64_t c = std::min(chunk, iters - done);
+        if (R > 0) c = std::min(c, R - (done % R));
+        return c;
+    };
+    SamplerPlan sp;
+    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, chunk, &sp,
+                               spec.kind == PCDM_SAMPLING_INDEPENDENT)) != PCDM_OK)
+        return s;
+    SamplingDev sdev;
+    if ((s = sampling_dev(spec, &p->du_T, &p->du_cap, st, &sdev)) != PCDM_OK) return s;
+    // host x: every sample set of the run is drawn on a side stream while x crosses PCIe
+    // (the sampler needs only seed and k; the copy engines and the SMs overlap)
+    const char* pe = getenv("PCDM_PRESAMPLE");
+    const bool presample = !x_dev && iters > 0 && spec.kind == PCDM_SAMPLING_NICE && !(pe && atoi(pe) == 0) &&
+                           (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
+    if (presample) {
+        const size_t need = sizeof(int) * (size_t)iters * (size_t)tau;
+        if (p->pre_cap < need) {
+            cudaFree(p->pre_slots);
+            p->pre_slots = nullptr;
+            p->pre_cap = 0;
+            CK(cudaMalloc((void**)&p->pre_slots, need), "alloc presampled slots");
+            p->pre_cap = need;
+        }
+        if (!p->side) {
+            CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking), "side stream");
+            CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "event");
+            CK(cudaEventCreate(&p->ev_s0), "event");
+            CK(cudaEventCreate(&p->ev_s1), "event");
+        }
+        CK(cudaEventRecord(p->ev_fork, st), "event");
+        CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0), "event");
+        CK(cudaEventRecord(p->ev_s0, p->side), "event");
+        CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), p->side), "memset rounds");
+        for (int64_t done = 0; done < iters;) {
+            const int64_t c = chunk_len(done);
+            CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, p->pre_slots + done * tau, &p->sc->flags, p->side,
+                            p->sms, &launches),
+               "sampler");
+            done += c;
+        }
+        CK(cudaEventRecord(p->ev_s1, p->side), "event");
+    } else {
+        CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), st), "memset rounds");
+    }
     float* xd = x;
     if (!x_dev) {
         if (!p->xbuf) CK(cudaMalloc((void**)&p->xbuf, sizeof(float) * p->n), "alloc x buffer");
         CK(cudaMemcpyAsync(p->xbuf, x, sizeof(float) * p->n, cudaMemcpyHostToDevice, st), "copy x in");
         xd = p->xbuf;
     }
-    CK(cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st), "memset scalars");
-    pcdm_status s = PCDM_OK;
-    Scalars hs{};
 
     double beta_d = sampling_beta(spec, p->omega, p->n);
     if (beta_override > 0.0) beta_d = beta_override;
-    const int64_t R = refresh_period(p->n, tau, refresh_every);
     IterLaunch plan = plan_iter(variant >= PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
                                 p->sms, p->device, p->loss == 1);
     // AUTO: packed blocks whenever the shared-memory variant does not apply
@@ -760,15 +822,6 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                "x headers");
         return PCDM_OK;
     };
-    int64_t chunk = choose_chunk(p->n, tau, iters);
-    if (R > 0) chunk = std::min(chunk, R);
-    SamplerPlan sp;
-    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, chunk, &sp,
-                               spec.kind == PCDM_SAMPLING_INDEPENDENT)) != PCDM_OK)
-        return s;
-    CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), st), "memset rounds");
-    SamplingDev sdev;
-    if ((s = sampling_dev(spec, &p->du_T, &p->du_cap, st, &sdev)) != PCDM_OK) return s;
 
     IterParams P{};
     P.colptr = p->colptr;
@@ -906,14 +959,16 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.ctas = cl_size;
     }
 
+    if (presample) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
     int64_t done = 0;
     while (done < iters) {
-        int64_t c = std::min(chunk, iters - done);
-        if (R > 0) c = std::min(c, R - (done % R));
+        const int64_t c = chunk_len(done);
+        int* slots_c = presample ? p->pre_slots + done * tau : sp.slots;
         int ts;
         CK(tm.begin(&ts), "event");
-        CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
-           "sampler");
+        if (!presample)
+            CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
+               "sampler");
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
         CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed || batched ? 0 : 3 * sizeof(int)), st),
@@ -923,21 +978,21 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         int ti;
         CK(tm.begin(&ti), "event");
         if (clustered) {
-            CP.slots = sp.slots;
+            CP.slots = slots_c;
             CP.iters = c;
             CK(launch_cluster(p->packed_G, cl_size, CP, cl_smem, st, &launches), "cluster iteration kernel");
         } else if (batched) {
-            B.slots = sp.slots;
+            B.slots = slots_c;
             B.iters = c;
             B.nq = (int)((c * tau + (1ll << B.cq_log) - 1) >> B.cq_log);
             CK(launch_batched(p->packed_G, B, bat_ctas, st, p->sms, &launches), "batched iteration kernels");
         } else if (packed) {
-            Q.slots = sp.slots;
+            Q.slots = slots_c;
             Q.iters = c;
             Q.k0 = done;
             CK(launch_packed(p->packed_G, one_barrier, plan.ctas, Q, st, &launches), "packed iteration kernel");
         } else {
-            P.slots = sp.slots;
+            P.slots = slots_c;
             P.iters = c;
             CK(launch_iter(plan, P, st, &launches), "iteration kernel");
         }
@@ -1019,6 +1074,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     tm.sum(tms);
     stats.iter_kernel_ms = tms[T_ITER];
     stats.sampler_ms = tms[T_SAMPLER];
+    if (presample) {
+        float pms = 0.f;
+        if (cudaEventElapsedTime(&pms, p->ev_s0, p->ev_s1) == cudaSuccess) stats.sampler_ms += pms;
+        cudaGetLastError();
+    }
     stats.setup_ms = tms[T_SETUP];
     p->stats = stats;
     if (hs.flags & FLAG_SAMPLER) return fail(PCDM_ESAMPLER, "sampler round counter overflow");
