@@ -283,7 +283,7 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
         if (e != cudaSuccess) return e;
         sample_round0_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
         sample_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
-        sample_rounds_kernel<<<(unsigned)count, 256, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
+        sample_rounds_kernel<<<(unsigned)count, 1024, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
                                                                w.rounds_max, flags);
         *launches += 3;
         e = cudaGetLastError();
