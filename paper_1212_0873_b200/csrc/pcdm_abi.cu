@@ -960,6 +960,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
 
     if (presample) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
+    bool list_restarted = false;
     int64_t done = 0;
     while (done < iters) {
         const int64_t c = chunk_len(done);
@@ -1003,7 +1004,19 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             int tr;
             CK(tm.begin(&tr), "event");
             if ((s = x_out()) != PCDM_OK) return s;  // the refresh reads x
-            if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) return s;
+            if (xhdr) {
+                // restart the dirty list from the support of x (the refresh pass re-lists the
+                // nonzero x_i), so it does not grow with every step of a long run; the host
+                // copy-back then cannot name entries that became zero: it copies all of x
+                CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap, p->n, st, p->sms,
+                                     &launches),
+                   "x headers");
+                CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
+                list_restarted = true;
+                if ((s = residual_from(p, xd, st, &launches, &xh)) != PCDM_OK) return s;
+            } else if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) {
+                return s;
+            }
             if (one_barrier) {
                 CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
                 CK(cudaMemsetAsync(p->sc->nz_count, 0, 3 * sizeof(int), st), "memset lists");
@@ -1022,7 +1035,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         // changed: copy back (index, value) pairs when that is less than the whole x
         bool compact = false;
         unsigned long long cnt = 0;
-        if (xhdr) {
+        if (xhdr && !list_restarted) {
             CK(cudaMemcpyAsync(&cnt, p->xlist_count, sizeof(cnt), cudaMemcpyDeviceToHost, st), "read x list");
             CK(cudaStreamSynchronize(st), "stream synchronize");
             compact = cnt <= (unsigned long long)p->xlist_cap && 8 * (int64_t)cnt < 4 * p->n;

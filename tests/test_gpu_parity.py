@@ -375,8 +375,8 @@ def test_caller_changes_x_between_runs(gpu):
 
 
 # ------------------------------------------------------------------ host x: compact copy-back
-@pytest.mark.parametrize("cap", [None, "3"], ids=["compact", "list-overflow"])
-def test_host_x_compact_copy_back(gpu, monkeypatch, cap):
+@pytest.mark.parametrize("cap,refresh", [(None, 0), ("3", 0), (None, 9)], ids=["compact", "list-overflow", "refresh"])
+def test_host_x_compact_copy_back(gpu, monkeypatch, cap, refresh):
     # packed loop with x in the block headers: only the dirty entries travel back to the host
     if cap:
         monkeypatch.setenv("PCDM_XLIST_CAP", cap)
@@ -387,16 +387,16 @@ def test_host_x_compact_copy_back(gpu, monkeypatch, cap):
     prob = pcdm.Problem(m, n, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), lam)
     xh = x0.copy()
     xd = torch.from_numpy(x0.copy()).to(gpu)
-    prob.run(xh, 256, 40, seed=9, variant="packed")
+    prob.run(xh, 256, 40, seed=9, variant="packed", refresh_every=refresh)
     st = prob.stats()
-    prob.run(xd, 256, 40, seed=9, variant="packed")
+    prob.run(xd, 256, 40, seed=9, variant="packed", refresh_every=refresh)
     np.testing.assert_allclose(xh, to_host(xd), rtol=1e-5, atol=1e-6)
     assert st["host_h2d_bytes"] == 4 * n
-    if cap:
+    if cap or refresh:  # an overflowed or restarted dirty list: the whole x travels back
         assert st["host_d2h_bytes"] == 4 * n
     else:
         assert 0 < st["host_d2h_bytes"] < 4 * n // 4
     xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), lam, 256, 40, 9,
-                    x0=x0.astype(np.float64)).x
+                    x0=x0.astype(np.float64), refresh_every=refresh).x
     assert np.max(np.abs(xh - xo)) <= 1e-4 * np.max(np.abs(xo))
     prob.close()
