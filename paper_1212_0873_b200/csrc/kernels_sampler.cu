@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -35,6 +36,7 @@ struct DrawArgs {
     int log2h;
 };
 
+template <bool CAS_FIRST>
 __global__ void sample_round0_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables,
                                      int* cand) {
     const int64_t total = count * a.cnt;
@@ -44,7 +46,10 @@ __global__ void sample_round0_kernel(DrawArgs a, int64_t k0, int64_t count, unsi
         const uint32_t j = (uint32_t)(t - it * a.cnt);
         const long long v = draw_value(a.seed, (uint32_t)(k0 + it), 0u, j, a.tag, a.n, a.reject_below);
         cand[t] = (int)v;
-        if (v >= 0) table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+        if (v >= 0) {
+            if (CAS_FIRST) table_insert_cas_first(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+            else table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+        }
     }
 }
 
@@ -281,7 +286,15 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(w.npending, 0, (size_t)count * sizeof(int), st);
         if (e != cudaSuccess) return e;
-        sample_round0_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
+        // CAS straight on the home entry (the tables were just cleared): huge sampler
+        // 8.23 -> 7.05 ms/step, large 8.80 -> 7.68 (profiles/r01_sampler_cas_first_ab.jsonl);
+        // PCDM_CAS_FIRST=0 restores load-then-CAS
+        static const bool cas_first = [] {
+            const char* v = getenv("PCDM_CAS_FIRST");
+            return !(v && atoi(v) == 0);
+        }();
+        if (cas_first) sample_round0_kernel<true><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
+        else sample_round0_kernel<false><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
         sample_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
         sample_rounds_kernel<<<(unsigned)count, 1024, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
                                                                w.rounds_max, flags);
