@@ -159,17 +159,19 @@ __device__ __forceinline__ void table_insert(unsigned long long* table, int log2
 
 // Same result as table_insert, starting with the CAS on the home entry (no load
 // first): one L2 operation per insert when the home entry is empty.
-__device__ __forceinline__ void table_insert_cas_first(unsigned long long* table, int log2h, uint32_t v,
-                                                       uint32_t code) {
+// Returns the entry index the value occupies (values never move: linear probing
+// without deletion).
+__device__ __forceinline__ uint32_t table_insert_cas_first(unsigned long long* table, int log2h, uint32_t v,
+                                                           uint32_t code) {
     const unsigned long long key = ((unsigned long long)v << 32) | code;
     const uint32_t mask = (1u << log2h) - 1u;
     uint32_t h = hash_slot(v, log2h);
     while (true) {
         const unsigned long long prev = atomicCAS(&table[h], PCDM_EMPTY_SLOT, key);
-        if (prev == PCDM_EMPTY_SLOT) return;
+        if (prev == PCDM_EMPTY_SLOT) return h;
         if ((uint32_t)(prev >> 32) == v) {
             atomicMin(&table[h], key);
-            return;
+            return h;
         }
         h = (h + 1) & mask;
     }

@@ -11,9 +11,10 @@
 // Device realisation: round 0 for every (iteration, slot) of a chunk is one
 // grid-wide pass inserting (value, code = rho*cnt + j) into a per-iteration
 // open-addressing table that keeps the minimum code per value (64-bit
-// atomicMin on (value << 32 | code)); a second pass keeps the owners; the few
-// leftover slots finish their rounds inside one CTA per iteration.  The result
-// depends only on the codes, never on thread timing.
+// atomicMin on (value << 32 | code); the insert CASes the home entry first and
+// records the entry the value landed in); a second pass keeps the owners by
+// reading that entry; the few leftover slots finish their rounds inside one CTA
+// per iteration.  The result depends only on the codes, never on thread timing.
 #include <cub/block/block_scan.cuh>
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
@@ -38,7 +39,7 @@ struct DrawArgs {
 
 template <bool CAS_FIRST>
 __global__ void sample_round0_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables,
-                                     int* cand) {
+                                     int* cand, int* pending) {
     const int64_t total = count * a.cnt;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -47,12 +48,19 @@ __global__ void sample_round0_kernel(DrawArgs a, int64_t k0, int64_t count, unsi
         const long long v = draw_value(a.seed, (uint32_t)(k0 + it), 0u, j, a.tag, a.n, a.reject_below);
         cand[t] = (int)v;
         if (v >= 0) {
-            if (CAS_FIRST) table_insert_cas_first(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
-            else table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+            if (CAS_FIRST) {
+                // the entry index goes to the (still unused) second half of the iteration's
+                // pending area, so the check pass reads one entry instead of probing
+                const uint32_t at = table_insert_cas_first(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+                if (pending) pending[it * 2 * a.cnt + a.cnt + j] = (int)at;
+            } else {
+                table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+            }
         }
     }
 }
 
+template <bool AT>
 __global__ void sample_check_kernel(DrawArgs a, int64_t count, const unsigned long long* tables,
                                     const int* cand, int* pending, int* npending) {
     const int64_t total = count * a.cnt;
@@ -61,7 +69,10 @@ __global__ void sample_check_kernel(DrawArgs a, int64_t count, const unsigned lo
         const int64_t it = t / a.cnt;
         const uint32_t j = (uint32_t)(t - it * a.cnt);
         const int v = cand[t];
-        const bool owned = v >= 0 && table_owner(tables + (it << a.log2h), a.log2h, (uint32_t)v) == j;
+        const unsigned long long* table = tables + (it << a.log2h);
+        const bool owned =
+            v >= 0 && (AT ? (uint32_t)__ldcg(table + pending[it * 2 * a.cnt + a.cnt + j]) == j
+                          : table_owner(table, a.log2h, (uint32_t)v) == j);
         if (!owned) {
             const int pos = atomicAdd(npending + it, 1);
             pending[it * 2 * a.cnt + pos] = (int)j;
@@ -293,9 +304,22 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
             const char* v = getenv("PCDM_CAS_FIRST");
             return !(v && atoi(v) == 0);
         }();
-        if (cas_first) sample_round0_kernel<true><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
-        else sample_round0_kernel<false><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand);
-        sample_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
+        // round 0 records where each value landed, so the check pass reads that entry
+        // instead of probing (huge sampler 7.57 -> 6.03 ms/step,
+        // profiles/r01_sampler_check_at_ab.jsonl); PCDM_CHECK_AT=0 probes
+        static const bool rec_at = [] {
+            const char* v = getenv("PCDM_CHECK_AT");
+            return !(v && atoi(v) == 0);
+        }();
+        if (cas_first) {
+            sample_round0_kernel<true><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand, rec_at ? w.pending : nullptr);
+        } else {
+            sample_round0_kernel<false><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand, nullptr);
+        }
+        if (cas_first && rec_at)
+            sample_check_kernel<true><<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
+        else
+            sample_check_kernel<false><<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
         sample_rounds_kernel<<<(unsigned)count, 1024, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
                                                                w.rounds_max, flags);
         *launches += 3;
