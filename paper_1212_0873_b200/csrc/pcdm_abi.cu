@@ -102,6 +102,8 @@ struct pcdm_problem {
     int* hidx = nullptr;       // pinned host staging of the compact copy (indices, values)
     float* hval = nullptr;
     int64_t comp_cap = 0;
+    int* slot_buf = nullptr;   // slot arrays of one iteration-kernel launch (when it spans several sampler chunks)
+    size_t slot_cap = 0;
     int* pre_slots = nullptr;  // host-x runs: the whole run's slot arrays, drawn during the x copy
     size_t pre_cap = 0;
     cudaStream_t side = nullptr;
@@ -151,6 +153,7 @@ void free_problem(pcdm_problem* p) {
     cudaFreeHost(p->hidx);
     cudaFreeHost(p->hval);
     cudaFree(p->pre_slots);
+    cudaFree(p->slot_buf);
     if (p->side) {
         cudaStreamDestroy(p->side);
         cudaEventDestroy(p->ev_fork);
@@ -960,16 +963,42 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
 
     if (presample) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
+    // iterations per launch of the iteration kernel: up to 64 (PCDM_ITER_CHUNK), each
+    // launch's slots drawn in sampler chunks of `chunk` iterations; fewer launches of the
+    // persistent kernel (each costs its ramp-up and drain)
+    int64_t ichunk = chunk;
+    if (!batched) {
+        int64_t want = 64;
+        if (const char* ic = getenv("PCDM_ITER_CHUNK")) want = std::max<int64_t>(1, atoll(ic));
+        ichunk = std::max(chunk, std::min(want, iters));
+        if (R > 0) ichunk = std::min(ichunk, R);
+    }
+    const bool own_slots = !presample && ichunk > chunk;
+    if (own_slots && p->slot_cap < (size_t)(ichunk * tau)) {
+        cudaFree(p->slot_buf);
+        p->slot_buf = nullptr;
+        p->slot_cap = 0;
+        CK(cudaMalloc((void**)&p->slot_buf, sizeof(int) * ichunk * tau), "alloc slot buffer");
+        p->slot_cap = (size_t)(ichunk * tau);
+    }
+    auto iter_len = [&](int64_t done) {
+        int64_t c = std::min(ichunk, iters - done);
+        if (R > 0) c = std::min(c, R - (done % R));
+        return c;
+    };
     bool list_restarted = false;
     int64_t done = 0;
     while (done < iters) {
-        const int64_t c = chunk_len(done);
-        int* slots_c = presample ? p->pre_slots + done * tau : sp.slots;
+        const int64_t c = iter_len(done);
+        int* slots_c = presample ? p->pre_slots + done * tau : (own_slots ? p->slot_buf : sp.slots);
         int ts;
         CK(tm.begin(&ts), "event");
-        if (!presample)
-            CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, sp.slots, &p->sc->flags, st, p->sms, &launches),
-               "sampler");
+        if (!presample) {
+            for (int64_t s0 = 0; s0 < c; s0 += chunk)
+                CK(sample_chunk(sp.w, sdev, seed, first_iter + done + s0, std::min(chunk, c - s0), slots_c + s0 * tau,
+                                &p->sc->flags, st, p->sms, &launches),
+                   "sampler");
+        }
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
         CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed || batched ? 0 : 3 * sizeof(int)), st),
@@ -1081,7 +1110,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     stats.grid_ctas = plan.ctas;
     stats.threads_per_cta = plan.threads;
     stats.lanes_per_column = plan.lanes;
-    stats.chunk_iters = chunk;
+    stats.chunk_iters = ichunk;
     stats.hot_rows = packed && Q.hot_cache ? p->nhot : 0;
     double tms[3];
     tm.sum(tms);

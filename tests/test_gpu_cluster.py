@@ -60,6 +60,7 @@ def test_cluster_matches_oracle(gpu, lens_kind):
 def test_cluster_x_storage_chunks_and_hot_rows(gpu, monkeypatch, x_in_block):
     monkeypatch.setenv("PCDM_X_IN_BLOCK", x_in_block)
     monkeypatch.setenv("PCDM_CHUNK", "7")
+    monkeypatch.setenv("PCDM_ITER_CHUNK", "7")
     inst = I.generate(I.InstanceConfig("zipf_small", 20_000, 20_000, 20, 200, rows="zipf"), seed=0)
     for tau, iters in ((2048, 60), (200, 200)):
         out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, tau, iters, seed=tau,

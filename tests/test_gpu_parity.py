@@ -280,15 +280,18 @@ def test_packed_rejected_for_long_columns(gpu):
 
 
 # ------------------------------------------------------------------ many launches per run
+@pytest.mark.parametrize("iter_chunk", ["3", "16"], ids=["launch-per-sampler-chunk", "launch-spans-chunks"])
 @pytest.mark.parametrize("variant", ["packed", "grid"])
-def test_many_chunks_per_run(gpu, monkeypatch, variant):
-    # small chunks force many sampler passes and iteration-kernel launches per run
+def test_many_chunks_per_run(gpu, monkeypatch, variant, iter_chunk):
+    # small sampler chunks force many sampler passes per run; iteration-kernel launches
+    # of 3 iterations, or of 16 whose slots come from several sampler chunks
     monkeypatch.setenv("PCDM_CHUNK", "3")
+    monkeypatch.setenv("PCDM_ITER_CHUNK", iter_chunk)
     c, r, v, b, lam = _ragged(3000, 2500, np.full(2500, 12), 12)
     for tau, iters, refresh in ((256, 61, 0), (2500, 7, 4), (33, 200, -1)):
         out = run_both(c, r, v, b, lam, 3000, tau, iters, seed=5, variant=variant, refresh_every=refresh)
         assert_parity(out)
-        assert out["stats"]["iter_launches"] >= iters // 3
+        assert out["stats"]["iter_launches"] >= iters // int(iter_chunk)
 
 
 # ------------------------------------------------------------------ other DU samplings (NEXT-1)
