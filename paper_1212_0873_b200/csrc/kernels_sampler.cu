@@ -97,18 +97,26 @@ __global__ void sample_rounds_kernel(DrawArgs a, int64_t k0, unsigned long long*
             if (threadIdx.x == 0) atomicOr(flags, FLAG_SAMPLER);
             return;
         }
-        for (int t = threadIdx.x; t < np; t += blockDim.x) {
+        // the entry each of this thread's first kPos slots landed in (CAS-first insert)
+        constexpr int kPos = 4;
+        uint32_t at[kPos];
+        for (int t = threadIdx.x, q = 0; t < np; t += blockDim.x, ++q) {
             const uint32_t j = (uint32_t)pin[t];
             const long long v = draw_value(a.seed, (uint32_t)(k0 + it), rho, j, a.tag, a.n, a.reject_below);
             c[j] = (int)v;
-            if (v >= 0) table_insert(table, a.log2h, (uint32_t)v, rho * (uint32_t)a.cnt + j);
+            if (v >= 0) {
+                const uint32_t h = table_insert_cas_first(table, a.log2h, (uint32_t)v, rho * (uint32_t)a.cnt + j);
+                if (q < kPos) at[q] = h;
+            }
         }
         if (threadIdx.x == 0) s_next = 0;
         __syncthreads();
-        for (int t = threadIdx.x; t < np; t += blockDim.x) {
+        for (int t = threadIdx.x, q = 0; t < np; t += blockDim.x, ++q) {
             const uint32_t j = (uint32_t)pin[t];
             const int v = c[j];
-            const bool owned = v >= 0 && table_owner(table, a.log2h, (uint32_t)v) == rho * (uint32_t)a.cnt + j;
+            const uint32_t code = rho * (uint32_t)a.cnt + j;
+            const bool owned = v >= 0 && (q < kPos ? (uint32_t)__ldcg(table + at[q]) == code
+                                                   : table_owner(table, a.log2h, (uint32_t)v) == code);
             if (!owned) pout[atomicAdd(&s_next, 1)] = (int)j;
         }
         __syncthreads();
