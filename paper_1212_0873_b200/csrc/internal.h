@@ -31,8 +31,18 @@ struct XHeaders {
     unsigned long long* count;
     int64_t cap;
 };
+// Row-major copy of A (built for dense iterates: the logistic problem)
+struct DevCSR {
+    const int64_t* rowptr;  // [m+1]
+    const int* col;         // [nnz]
+    const float* val;       // [nnz]
+};
+// r64 = A x - b in fp64: column scatter with fp64 atomics, or (csr given) a warp per row
+// without atomics; both also copy nonzero x_i into the block headers when xh is given
 cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
-                              cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh = nullptr);
+                              cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh = nullptr,
+                              const DevCSR* csr = nullptr);
+cudaError_t build_csr(const DevCSC& A, const int* counts, DevCSR* out, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,
                            int64_t* launches);
 cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
@@ -131,6 +141,8 @@ struct PackedParams {
     int64_t xlist_cap;
     const int* hot_rows;  // [nhot] ascending row ids of the hot rows (block row field 0x80000000 | h)
     int nhot;             // 0: no hot rows (blocks hold plain row ids)
+    int list_cap;         // > 0: nonzero steps staged per CTA in shared memory (capacity), one
+                          //      global atomic per CTA and iteration (dense-step workloads)
     int hot_cache;        // 1: copy r_k[hot_rows] into shared memory every iteration (else
                           //    hot entries are gathered through the row table)
 };
@@ -164,10 +176,10 @@ cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStrea
 // rows listed in hot_rows[0..nhot) (ascending) are stored as 0x80000000 | h
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
                         const int* hot_rows, int nhot, int4* blocks, cudaStream_t st, int sms, int64_t* launches);
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false, int nhot = 0);
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false, int nhot = 0, int list_cap = 0);
 cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
                           int64_t* launches);
-size_t packed_smem_bytes(int nhot);
+size_t packed_smem_bytes(int nhot, int list_cap = 0);
 
 // ---- batched-snapshot loop (kernels_batched.cu): passes expand / sweep / steps / fold
 struct BatchedParams {

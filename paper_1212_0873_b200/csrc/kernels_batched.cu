@@ -351,8 +351,10 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_kernel(BatchedParams
                         if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
                         if (P.xlist) {
                             ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
-                            const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
-                            if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = i;
+                            if (P.xlist_cap > 0) {  // 0: dense iterate, no dirty list
+                                const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
+                                if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = i;
+                            }
                         } else {
                             P.x[i] = xp;
                         }

@@ -105,10 +105,17 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
     float* s_hot = s_dyn;                      // [nhot] r_k at the hot rows
     int* s_hrow = (int*)(s_dyn + P.nhot);      // [nhot] hot row ids
     const int nhot = P.nhot;
+    // staged step list (P.list_cap > 0): [list_cap] ids, [list_cap] steps, count, base
+    const bool stage = P.list_cap > 0;
+    int* s_li = s_hrow + nhot;
+    float* s_ld = (float*)(s_li + P.list_cap);
+    int* s_lc = (int*)(s_ld + P.list_cap);
+    int* s_lbase = s_lc + 1;
+    if (stage && threadIdx.x == 0) *s_lc = 0;
     const bool cache = P.hot_cache != 0;
     // CTAs without slots in an iteration skip the hot-row copy
     const bool has_slots = (int64_t)blockIdx.x * (kThreads / G) < tau;
-    if (nhot) {
+    if (nhot || stage) {
         for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
         __syncthreads();
     }
@@ -190,20 +197,40 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
                     if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
                     if (P.xlist) {
                         ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
-                        const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
-                        if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = i;
+                        if (P.xlist_cap > 0) {  // 0: dense iterate, no dirty list
+                            const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
+                            if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = i;
+                        }
                     } else {
                         P.x[i] = xp;
                     }
-                    const int pos = atomicAdd(P.nz_count + cur, 1);
-                    P.nz_idx[cur * tau + pos] = i;
-                    P.nz_delta[cur * tau + pos] = d;
+                    if (stage) {  // CTA-local list, flushed with one global atomic per CTA
+                        const int pos = atomicAdd(s_lc, 1);
+                        s_li[pos] = i;
+                        s_ld[pos] = d;
+                    } else {
+                        const int pos = atomicAdd(P.nz_count + cur, 1);
+                        P.nz_idx[cur * tau + pos] = i;
+                        P.nz_delta[cur * tau + pos] = d;
+                    }
                 }
             }
             if (ONE_BARRIER) {
                 d = __shfl_sync(gm, d, src);
                 if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
             }
+        }
+        if (stage) {
+            __syncthreads();
+            const int cnt = *s_lc;
+            if (threadIdx.x == 0 && cnt) *s_lbase = atomicAdd(P.nz_count + cur, cnt);
+            __syncthreads();
+            for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+                P.nz_idx[cur * tau + *s_lbase + e] = s_li[e];
+                P.nz_delta[cur * tau + *s_lbase + e] = s_ld[e];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) *s_lc = 0;  // ordered before the next appends by the barrier
         }
         if (ONE_BARRIER) {
             // the next iteration's first slot is loaded while the other CTAs arrive
@@ -379,7 +406,7 @@ template <int G, bool ONE, bool LOG>
 cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
     void* args[] = {(void*)&P};
     return cudaLaunchCooperativeKernel((const void*)pcdm_packed_kernel<G, ONE, LOG>, dim3(ctas), dim3(kThreads),
-                                       args, packed_smem_bytes(P.nhot), st);
+                                       args, packed_smem_bytes(P.nhot, P.list_cap), st);
 }
 
 template <bool ONE, bool LOG>
@@ -450,7 +477,9 @@ cudaError_t launch_gather_list(const float* x, const int* list, int64_t count, f
     return cudaGetLastError();
 }
 
-size_t packed_smem_bytes(int nhot) { return (size_t)nhot * (sizeof(float) + sizeof(int)); }
+size_t packed_smem_bytes(int nhot, int list_cap) {
+    return (size_t)nhot * (sizeof(float) + sizeof(int)) + (list_cap > 0 ? (size_t)list_cap * 8 + 8 : 0);
+}
 
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
                         const int* hot_rows, int nhot, int4* blocks, cudaStream_t st, int sms, int64_t* launches) {
@@ -489,11 +518,11 @@ cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st,
     return cudaGetLastError();
 }
 
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot) {
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot, int list_cap) {
     int per_sm = 1;
     const void* fn = logistic ? (one_barrier ? kernel_ptr<true, true>(G) : kernel_ptr<false, true>(G))
                               : (one_barrier ? kernel_ptr<true, false>(G) : kernel_ptr<false, false>(G));
-    const size_t smem = packed_smem_bytes(nhot);
+    const size_t smem = packed_smem_bytes(nhot, list_cap);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;

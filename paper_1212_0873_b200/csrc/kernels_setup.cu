@@ -2,6 +2,7 @@
 //   CSC validation, row histogram + omega, column norms
 //   L_i = ||a_i||^2, residual r = Ax - b (fp64 scratch), and
 //   the objective F = 1/2||r||^2 + lambda||x||_1 (eq:P).
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -10,6 +11,7 @@
 #include "internal.h"
 
 using namespace pcdm;
+using pcdm_internal::DevCSR;
 using pcdm_internal::XHeaders;
 
 namespace {
@@ -137,17 +139,60 @@ __device__ __forceinline__ void scatter_col(int64_t i, float xi, const long long
     }
     if (xh.blocks) {
         ((float*)(xh.blocks + i * xh.G))[2] = xi;
-        const unsigned long long q = atomicAdd(xh.count, 1ull);
-        if (q < (unsigned long long)xh.cap) xh.list[q] = (int)i;
+        if (xh.cap > 0) {  // 0: dense iterate, no dirty list
+            const unsigned long long q = atomicAdd(xh.count, 1ull);
+            if (q < (unsigned long long)xh.cap) xh.list[q] = (int)i;
+        }
     }
+    if (!colptr) return;
     const double xd = (double)xi;
     for (long long p = colptr[i]; p < colptr[i + 1]; ++p) atomicAdd(r64 + rowidx[p], (double)val[p] * xd);
 }
 
+// Row-major residual (dense iterates, e.g. the logistic margins): one warp per row,
+// r64_j = -b_j + sum_{(j,i) stored} a_ji x_i in fp64 registers, no atomics.
+__global__ void residual_rows_kernel(int64_t m, const long long* __restrict__ rowptr, const int* __restrict__ ccol,
+                                     const float* __restrict__ cval, const float* __restrict__ b,
+                                     const float* __restrict__ x, double* __restrict__ r64) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < m; j += nw) {
+        const long long s = rowptr[j], e = rowptr[j + 1];
+        double acc = 0.0;
+        for (long long q = s + lane; q < e; q += 32) acc += (double)cval[q] * (double)__ldg(x + ccol[q]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) r64[j] = acc - (double)b[j];
+    }
+}
+
+// CSR fill: entry (i, row, val) goes to the next free position of its row
+__global__ void csr_fill_kernel(int64_t n, const long long* __restrict__ colptr, const int* __restrict__ rowidx,
+                                const float* __restrict__ val, unsigned long long* __restrict__ cursor,
+                                int* __restrict__ ccol, float* __restrict__ cval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+        for (long long p = colptr[i] + lane; p < colptr[i + 1]; p += 32) {
+            const unsigned long long pos = atomicAdd(cursor + rowidx[p], 1ull);
+            ccol[pos] = (int)i;
+            cval[pos] = val[p];
+        }
+    }
+}
+
+__global__ void counts64_kernel(int64_t m, const int* __restrict__ counts, unsigned long long* __restrict__ out) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = j < m ? (unsigned long long)counts[j] : 0ull;
+}
+
+// scatter = false: only the header copy / dirty list / non-finite check (the row-major
+// residual below computes r64 without atomics)
 __global__ void scatter_x_kernel(int64_t n, const long long* __restrict__ colptr,
                                  const int* __restrict__ rowidx, const float* __restrict__ val,
                                  const float* __restrict__ x, double* __restrict__ r64,
-                                 int* __restrict__ flags, XHeaders xh) {
+                                 int* __restrict__ flags, XHeaders xh, bool scatter) {
+    if (!scatter) colptr = nullptr;
     int bad = 0;
     const int64_t n4 = ((uintptr_t)x % 16 == 0) ? n / 4 : 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -333,13 +378,63 @@ cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms
 }
 
 cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
-                              cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh) {
+                              cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh, const DevCSR* csr) {
     const XHeaders none{nullptr, 0, nullptr, nullptr, 0};
+    if (csr) {
+        scatter_x_kernel<<<grid_for((A.n + 3) / 4, kThreads, sms * 8), kThreads, 0, st>>>(
+            A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags, xh ? *xh : none, false);
+        residual_rows_kernel<<<grid_for(A.m * 32, kThreads, sms * 16), kThreads, 0, st>>>(
+            A.m, (const long long*)csr->rowptr, csr->col, csr->val, b, x, r64);
+        *launches += 2;
+        return cudaGetLastError();
+    }
     neg_b_kernel<<<grid_for(A.m, kThreads, sms * 8), kThreads, 0, st>>>(A.m, b, r64);
     scatter_x_kernel<<<grid_for((A.n + 3) / 4, kThreads, sms * 8), kThreads, 0, st>>>(
-        A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags, xh ? *xh : none);
+        A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags, xh ? *xh : none, true);
     *launches += 2;
     return cudaGetLastError();
+}
+
+cudaError_t build_csr(const DevCSC& A, const int* counts, DevCSR* out, cudaStream_t st, int sms, int64_t* launches) {
+    unsigned long long* rowptr = nullptr;
+    unsigned long long* cursor = nullptr;
+    int* ccol = nullptr;
+    float* cval = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cudaError_t e = cudaMalloc((void**)&rowptr, sizeof(unsigned long long) * (A.m + 1));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&cursor, sizeof(unsigned long long) * (A.m + 1));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&ccol, sizeof(int) * A.nnz);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&cval, sizeof(float) * A.nnz);
+    if (e == cudaSuccess) {
+        counts64_kernel<<<grid_for(A.m + 1, kThreads, sms * 8), kThreads, 0, st>>>(A.m, counts, cursor);
+        ++*launches;
+        e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cursor, rowptr, A.m + 1, st);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cursor, rowptr, A.m + 1, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(cursor, rowptr, sizeof(unsigned long long) * (A.m + 1), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) {
+        csr_fill_kernel<<<grid_for(A.n * 32, kThreads, sms * 16), kThreads, 0, st>>>(
+            A.n, (const long long*)A.colptr, A.rowidx, A.val, cursor, ccol, cval);
+        ++*launches;
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    cudaFree(cursor);
+    if (e != cudaSuccess) {
+        cudaFree(rowptr);
+        cudaFree(ccol);
+        cudaFree(cval);
+        cudaGetLastError();
+        return e;
+    }
+    out->rowptr = (const int64_t*)rowptr;
+    out->col = ccol;
+    out->val = cval;
+    return cudaSuccess;
 }
 
 cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,

@@ -91,6 +91,8 @@ struct pcdm_problem {
     int* hot_rows = nullptr;   // ascending ids of the hot rows cached in shared memory (packed loop)
     int nhot = 0;
     int64_t hot_max_count = 0; // stored entries of the most frequent row
+    DevCSR csr{};              // row-major copy of A (logistic problems: dense iterates)
+    bool has_csr = false;
     float* d0 = nullptr;       // BATCHED: D = r_k - r_0 double buffer (zero between chunks)
     float* d1 = nullptr;
     void* bat_mem = nullptr;   // BATCHED per-chunk workspace (g0, sorted entries, offsets, lists)
@@ -143,6 +145,11 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->r2);
     cudaFree(p->blocks);
     cudaFree(p->hot_rows);
+    if (p->has_csr) {
+        cudaFree((void*)p->csr.rowptr);
+        cudaFree((void*)p->csr.col);
+        cudaFree((void*)p->csr.val);
+    }
     cudaFree(p->d0);
     cudaFree(p->d1);
     cudaFree(p->bat_mem);
@@ -188,7 +195,9 @@ pcdm_status read_scalars(pcdm_problem* p, Scalars* host, cudaStream_t st) {
 // r <- A x - b with fp64 accumulation (x device pointer).
 pcdm_status residual_from(pcdm_problem* p, const float* x, cudaStream_t st, int64_t* launches,
                           const XHeaders* xh = nullptr) {
-    CK(launch_residual64(p->csc(), p->b, x, p->r64, &p->sc->flags, st, p->sms, launches, xh), "residual kernels");
+    CK(launch_residual64(p->csc(), p->b, x, p->r64, &p->sc->flags, st, p->sms, launches, xh,
+                         p->has_csr ? &p->csr : nullptr),
+       "residual kernels");
     CK(launch_round_r(p->m, p->r64, p->r, st, p->sms, launches), "residual rounding");
     return PCDM_OK;
 }
@@ -546,6 +555,14 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         if (e != cudaSuccess) { cudaFree(counts); s = cuda_fail(e, "row histogram"); break; }
         s = read_scalars(p, &hs, st);
         if (s == PCDM_OK) s = select_hot_rows(p, counts, st, &launches);
+        // logistic problems: every visited coordinate becomes nonzero, so the margins
+        // s = A~ x are recomputed at each run start / refresh from a row-major copy (a warp
+        // per row, fp64 in registers) instead of nnz fp64 atomics (PCDM_ROW_RESIDUAL=0: off)
+        const char* rr = getenv("PCDM_ROW_RESIDUAL");
+        if (s == PCDM_OK && loss == 1 && !(rr && atoi(rr) == 0)) {
+            if (build_csr(p->csc(), counts, &p->csr, st, p->sms, &launches) == cudaSuccess) p->has_csr = true;
+            else cudaGetLastError();  // out of memory: the column scatter stays
+        }
         cudaFree(counts);
         if (s != PCDM_OK) break;
         p->omega = hs.max_out;
@@ -756,6 +773,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const bool clustered = cl_size > 0;
     if (clustered) packed = false;
     bool one_barrier = false;
+    int list_cap = 0;
     if (packed) {
         // one barrier per iteration (double-buffered r, the previous iteration's steps
         // replayed): measured faster on every config (huge: 45.7 -> 44.2 ms/step,
@@ -781,6 +799,18 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             const int v = atoi(cs);
             if (v >= 1) plan.ctas = std::min(v, packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot));
         }
+        // dense-step workloads (logistic: every step is nonzero): stage each CTA's steps in
+        // shared memory, one atomic on the list counter per CTA instead of one per step
+        // (PCDM_STAGE_LIST=0/1 overrides)
+        const char* sl = getenv("PCDM_STAGE_LIST");
+        if (sl ? atoi(sl) != 0 : p->loss == 1) {
+            const int64_t groups = (int64_t)plan.ctas * plan.threads / p->packed_G;
+            const int64_t cap = ((tau + groups - 1) / groups) * (plan.threads / p->packed_G);
+            const int full = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot);
+            if (cap * 8 <= 32 * 1024 &&
+                packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, (int)cap) == full)
+                list_cap = (int)cap;
+        }
     }
     if (p->nz_cap < tau) {
         cudaFree(p->nz_idx);
@@ -797,7 +827,13 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // header load rides on the residual pass, which reads x anyway.
     const char* xib = getenv("PCDM_X_IN_BLOCK");
     const bool xhdr = (packed || batched || clustered) && !(xib && atoi(xib) == 0);
+    // dense iterates (logistic: every visited coordinate steps) keep no dirty list: its
+    // appends would all hit one counter; the header passes walk all n columns instead
+    // (list count pinned at ~0 = "overflowed", appends skipped with cap 0; PCDM_XLIST_DENSE)
+    const char* xde = getenv("PCDM_XLIST_DENSE");
+    const bool xdense = xde ? atoi(xde) != 0 : p->loss == 1;
     XHeaders xh{};
+    int64_t cap_eff = 0;
     if (xhdr) {
         if (!p->xlist) {
             int64_t cap = std::min<int64_t>(p->n, (int64_t)1 << 26);
@@ -810,8 +846,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap, p->n, st, p->sms,
                              &launches),
            "x headers");
-        CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
-        xh = XHeaders{p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap};
+        cap_eff = xdense ? 0 : p->xlist_cap;
+        CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
+        xh = XHeaders{p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff};
     }
     if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr)) != PCDM_OK) return s;
     if (one_barrier) CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
@@ -820,7 +857,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
     auto x_out = [&]() -> pcdm_status {
         if (xhdr)
-            CK(launch_xhdr_out(p->blocks, p->packed_G, xd, p->n, p->xlist, p->xlist_count, p->xlist_cap, st, p->sms,
+            CK(launch_xhdr_out(p->blocks, p->packed_G, xd, p->n, p->xlist, p->xlist_count, cap_eff, st, p->sms,
                                &launches),
                "x headers");
         return PCDM_OK;
@@ -862,9 +899,10 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.logistic = p->loss;
     Q.xlist = xhdr ? p->xlist : nullptr;
     Q.xlist_count = p->xlist_count;
-    Q.xlist_cap = p->xlist_cap;
+    Q.xlist_cap = cap_eff;
     Q.hot_rows = p->hot_rows;
     Q.nhot = p->nhot;
+    Q.list_cap = list_cap;
     // cache the hot rows when the hottest one is read >= 1024 times per iteration
     // (tau count_max / n); below that the per-iteration copy costs more than the
     // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;
@@ -926,7 +964,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         B.x = xd;
         B.xlist = xhdr ? p->xlist : nullptr;
         B.xlist_count = p->xlist_count;
-        B.xlist_cap = p->xlist_cap;
+        B.xlist_cap = cap_eff;
         B.hot_rows = p->hot_rows;
         B.nhot = p->nhot;
         B.logistic = p->loss;
@@ -949,7 +987,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CP.x = xd;
         CP.xlist = xhdr ? p->xlist : nullptr;
         CP.xlist_count = p->xlist_count;
-        CP.xlist_cap = p->xlist_cap;
+        CP.xlist_cap = cap_eff;
         CP.hot_rows = p->hot_rows;
         CP.nhot = p->nhot;
         CP.list_cap = cl_cap;
@@ -1037,10 +1075,10 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                 // restart the dirty list from the support of x (the refresh pass re-lists the
                 // nonzero x_i), so it does not grow with every step of a long run; the host
                 // copy-back then cannot name entries that became zero: it copies all of x
-                CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap, p->n, st, p->sms,
+                CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff, p->n, st, p->sms,
                                      &launches),
                    "x headers");
-                CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
+                CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
                 list_restarted = true;
                 if ((s = residual_from(p, xd, st, &launches, &xh)) != PCDM_OK) return s;
             } else if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) {
@@ -1067,7 +1105,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         if (xhdr && !list_restarted) {
             CK(cudaMemcpyAsync(&cnt, p->xlist_count, sizeof(cnt), cudaMemcpyDeviceToHost, st), "read x list");
             CK(cudaStreamSynchronize(st), "stream synchronize");
-            compact = cnt <= (unsigned long long)p->xlist_cap && 8 * (int64_t)cnt < 4 * p->n;
+            compact = cnt <= (unsigned long long)cap_eff && 8 * (int64_t)cnt < 4 * p->n;
         }
         if (compact && cnt > 0) {
             if (p->comp_cap < (int64_t)cnt) {
@@ -1239,7 +1277,7 @@ pcdm_status pcdm_objective(pcdm_problem* p, const float* x, double* F, void* str
     do {
         cudaError_t e = cudaMemsetAsync(&p->sc->flags, 0, sizeof(int), st);
         if (e != cudaSuccess) { s = cuda_fail(e, "memset"); break; }
-        if ((e = launch_residual64(p->csc(), p->b, xd, p->r64, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "residual"); break; }
+        if ((e = launch_residual64(p->csc(), p->b, xd, p->r64, &p->sc->flags, st, p->sms, &launches, nullptr, p->has_csr ? &p->csr : nullptr)) != cudaSuccess) { s = cuda_fail(e, "residual"); break; }
         if (p->loss == 0) {
             if ((e = launch_objective_sums(p->m, p->n, p->r64, xd, p->sc->sums, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "objective"); break; }
         } else if ((e = launch_objective_logistic(p->m, p->n, p->r64, xd, p->sc->sums, st, p->sms, &launches)) != cudaSuccess) {

@@ -403,3 +403,28 @@ def test_host_x_compact_copy_back(gpu, monkeypatch, cap, refresh):
                     x0=x0.astype(np.float64), refresh_every=refresh).x
     assert np.max(np.abs(xh - xo)) <= 1e-4 * np.max(np.abs(xo))
     prob.close()
+
+
+# ------------------------------------------------------------------ dense-step bookkeeping on LASSO
+@pytest.mark.parametrize("stage,dense", [("1", "0"), ("0", "1"), ("1", "1")])
+def test_staged_step_list_and_dense_x(gpu, monkeypatch, stage, dense):
+    # the logistic defaults (CTA-staged step lists, no dirty x list) forced on a LASSO
+    # problem with many nonzero steps (lambda = 0), both barrier schemes, refreshes
+    monkeypatch.setenv("PCDM_STAGE_LIST", stage)
+    monkeypatch.setenv("PCDM_XLIST_DENSE", dense)
+    m, n = 5000, 4000
+    c, r, v, b, lam = _ragged(m, n, np.random.default_rng(9).integers(1, 30, size=n), 19)
+    x0 = np.random.default_rng(4).normal(size=n) * (np.arange(n) % 5 == 0)
+    for one_barrier in ("1", "0"):
+        monkeypatch.setenv("PCDM_ONE_BARRIER", one_barrier)
+        for tau, iters, refresh, lam_ in ((512, 120, 0, 0.0), (4000, 8, 3, lam), (64, 200, 0, lam)):
+            out = run_both(c, r, v, b, lam_, m, tau, iters, seed=tau, variant="packed", x0=x0, refresh_every=refresh)
+            assert_parity(out)
+    # host x with a dense list: the whole x travels back
+    prob = pcdm.Problem(m, n, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), 0.0)
+    xh = np.zeros(n, dtype=np.float32)
+    prob.run(xh, 512, 30, seed=1, variant="packed")
+    assert prob.stats()["host_d2h_bytes"] == (4 * n if dense == "1" else prob.stats()["host_d2h_bytes"])
+    xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), 0.0, 512, 30, 1).x
+    assert np.max(np.abs(xh - xo)) <= 1e-4 * np.max(np.abs(xo))
+    prob.close()
