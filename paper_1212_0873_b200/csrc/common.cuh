@@ -61,23 +61,26 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // ---------------------------------------------------------------- grid barrier
 // Monotone-counter barrier for a co-resident (cooperative) grid.  `target`
 // advances by gridDim.x per call; the counter is zeroed before each launch.
-// Release: __syncthreads + gpu-scope fence before the arrival; acquire: gpu-scope
-// load-acquire spin then fence, then __syncthreads to release the CTA.
-__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& target) {
+// Arrive: __syncthreads, then thread 0's red.release.gpu (cumulative over the
+// CTA's writes that __syncthreads ordered before it); wait: thread 0 spins with
+// ld.acquire.gpu, then __syncthreads releases the CTA.  No sequentially consistent
+// fences (-DPCDM_SC_BARRIER restores the __threadfence + atomicAdd form).  Work
+// issued between arrive and wait overlaps the other CTAs' arrival (it must not
+// write anything the barrier is meant to publish).
+#ifndef PCDM_SC_BARRIER
+__device__ __forceinline__ void grid_arrive(unsigned* counter, unsigned& target) {
     __syncthreads();
     target += gridDim.x;
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+}
+__device__ __forceinline__ void grid_wait(const unsigned* counter, unsigned target) {
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(counter, 1u);
         while ((int)(ld_acquire_u32(counter) - target) < 0) {
         }
-        __threadfence();
     }
     __syncthreads();
 }
-
-// Split form: work issued between arrive and wait overlaps the other CTAs' arrival
-// (it must not write anything the barrier is meant to publish).
+#else
 __device__ __forceinline__ void grid_arrive(unsigned* counter, unsigned& target) {
     __syncthreads();
     target += gridDim.x;
@@ -93,6 +96,11 @@ __device__ __forceinline__ void grid_wait(const unsigned* counter, unsigned targ
         __threadfence();
     }
     __syncthreads();
+}
+#endif
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& target) {
+    grid_arrive(counter, target);
+    grid_wait(counter, target);
 }
 
 // ---------------------------------------------------------------- Philox4x32-10
