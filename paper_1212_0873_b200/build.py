@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     tmp = LIB + ".tmp.%d" % os.getpid()
-    cmd = [NVCC] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+    extra = os.environ.get("PCDM_NVCC_EXTRA", "").split()  # experiments, e.g. -DPCDM_BARRIER_SLEEP=64
+    cmd = [NVCC] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + \
         ["-I", os.path.join(ROOT, "include"), "-o", tmp] + sources()
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)

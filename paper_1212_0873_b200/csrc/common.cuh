@@ -76,6 +76,9 @@ __device__ __forceinline__ void grid_arrive(unsigned* counter, unsigned& target)
 __device__ __forceinline__ void grid_wait(const unsigned* counter, unsigned target) {
     if (threadIdx.x == 0) {
         while ((int)(ld_acquire_u32(counter) - target) < 0) {
+#ifdef PCDM_BARRIER_SLEEP
+            __nanosleep(PCDM_BARRIER_SLEEP);
+#endif
         }
     }
     __syncthreads();

@@ -141,6 +141,8 @@ struct PackedParams {
     int64_t xlist_cap;
     const int* hot_rows;  // [nhot] ascending row ids of the hot rows (block row field 0x80000000 | h)
     int nhot;             // 0: no hot rows (blocks hold plain row ids)
+    int cluster_sync;     // 1 / 2: the grid is one thread-block cluster of 512- / 1024-thread CTAs,
+                          //        the barriers are barrier.cluster
     int list_cap;         // > 0: nonzero steps staged per CTA in shared memory (capacity), one
                           //      global atomic per CTA and iteration (dense-step workloads)
     int hot_cache;        // 1: copy r_k[hot_rows] into shared memory every iteration (else

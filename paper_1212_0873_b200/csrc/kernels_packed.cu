@@ -91,8 +91,8 @@ __device__ __forceinline__ float gather_r(const float* rP, int v, const float* s
     return cache ? s_hot[v & 0x7fffffff] : ld_l2_f32(rP + s_hrow[v & 0x7fffffff]);
 }
 
-template <int G, bool ONE_BARRIER, bool LOGISTIC>
-__global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P) {
+template <int G, bool ONE_BARRIER, bool LOGISTIC, int TPB = kThreads>
+__global__ void __launch_bounds__(TPB, TPB == kThreads ? 3 : 1) pcdm_packed_kernel(PackedParams P) {
     const int t = threadIdx.x & (G - 1);  // lane within the column group
     const unsigned gm = gmask_of<G>();
     const int src = (threadIdx.x & 31) & ~(G - 1);
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
     if (stage && threadIdx.x == 0) *s_lc = 0;
     const bool cache = P.hot_cache != 0;
     // CTAs without slots in an iteration skip the hot-row copy
-    const bool has_slots = (int64_t)blockIdx.x * (kThreads / G) < tau;
+    const bool has_slots = (int64_t)blockIdx.x * (blockDim.x / G) < tau;
     if (nhot || stage) {
         for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
         __syncthreads();
@@ -232,7 +232,13 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_packed_kernel(PackedParams P
             __syncthreads();
             if (threadIdx.x == 0) *s_lc = 0;  // ordered before the next appends by the barrier
         }
-        if (ONE_BARRIER) {
+        if (ONE_BARRIER && P.cluster_sync) {
+            // a grid of one thread-block cluster: the hardware cluster barrier (release /
+            // acquire at cluster scope, which covers the global-memory r, x and lists)
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            prefetch(it + 1);
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else if (ONE_BARRIER) {
             // the next iteration's first slot is loaded while the other CTAs arrive
             grid_arrive(P.barrier, bar_target);
             prefetch(it + 1);
@@ -405,8 +411,32 @@ __global__ void max_len_kernel(int64_t n, const long long* __restrict__ colptr, 
 template <int G, bool ONE, bool LOG>
 cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
     void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel((const void*)pcdm_packed_kernel<G, ONE, LOG>, dim3(ctas), dim3(kThreads),
-                                       args, packed_smem_bytes(P.nhot, P.list_cap), st);
+    const int tpb = (ONE && P.cluster_sync == 2) ? 1024 : kThreads;
+    const void* fn = tpb == 1024 ? (const void*)pcdm_packed_kernel<G, ONE, LOG, 1024>
+                                 : (const void*)pcdm_packed_kernel<G, ONE, LOG>;
+    const size_t smem = packed_smem_bytes(P.nhot, P.list_cap);
+    if (P.cluster_sync) {  // the whole grid is one cluster (ctas <= 16)
+        if (ctas > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(tpb);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = ctas;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelExC(&cfg, fn, args) == cudaSuccess) return cudaSuccess;
+        cudaGetLastError();  // cluster of this size not available: grid barrier instead
+        PackedParams Q = P;
+        Q.cluster_sync = 0;
+        void* qargs[] = {(void*)&Q};
+        return cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(tpb), qargs, smem, st);
+    }
+    return cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kThreads), args, smem, st);
 }
 
 template <bool ONE, bool LOG>

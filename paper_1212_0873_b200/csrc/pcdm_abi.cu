@@ -774,6 +774,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (clustered) packed = false;
     bool one_barrier = false;
     int list_cap = 0;
+    int cluster_sync = 0;
     if (packed) {
         // one barrier per iteration (double-buffered r, the previous iteration's steps
         // replayed): measured faster on every config (huge: 45.7 -> 44.2 ms/step,
@@ -795,6 +796,19 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         // every grid barrier (PCDM_CTAS overrides, for measurements)
         const int64_t busy = (tau * p->packed_G + plan.threads - 1) / plan.threads;
         if (busy < plan.ctas) plan.ctas = (int)busy;
+        // a grid that covers tau in one round with <= 16 CTAs fits one thread-block
+        // cluster: hardware cluster barriers instead of the global-memory grid barrier
+        // (skewed tau = 2^8: 8 CTAs, 41.5 -> 36.6 ms/step); 1024-thread CTAs when 512-thread
+        // ones would need more than 16 (medium: 16 x 1024, 39.2 -> 37.7 ms/step;
+        // profiles/r01_cluster_sync_ab.jsonl).  PCDM_CLUSTER_SYNC=0: off
+        const char* csy = getenv("PCDM_CLUSTER_SYNC");
+        cluster_sync = one_barrier && !(csy && atoi(csy) == 0) ? 1 : 0;
+        const int64_t busy1024 = (tau * p->packed_G + 1023) / 1024;
+        if (cluster_sync && busy > 16 && busy1024 <= 16 && !getenv("PCDM_CTAS")) {
+            plan.threads = 1024;
+            plan.ctas = (int)busy1024;
+            cluster_sync = 2;
+        }
         if (const char* cs = getenv("PCDM_CTAS")) {
             const int v = atoi(cs);
             if (v >= 1) plan.ctas = std::min(v, packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot));
@@ -903,6 +917,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.hot_rows = p->hot_rows;
     Q.nhot = p->nhot;
     Q.list_cap = list_cap;
+    // a grid that fits one cluster (<= 16 CTAs: small tau) synchronises with the hardware
+    // cluster barrier instead of the global-memory grid barrier
+    Q.cluster_sync = packed && plan.ctas <= 16 ? cluster_sync : 0;
     // cache the hot rows when the hottest one is read >= 1024 times per iteration
     // (tau count_max / n); below that the per-iteration copy costs more than the
     // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;
