@@ -676,15 +676,14 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Scalars hs{};
     // sampler plan: chunks of iterations, aligned with the residual refreshes
     const int64_t R = refresh_period(p->n, tau, refresh_every);
-    int64_t chunk = choose_chunk(p->n, tau, iters);
+    // schunk: iterations per sampler pass (its hash tables fit the workspace budget);
+    // chunk: the same capped at the refresh period (the BATCHED workspace unit)
+    const int64_t schunk = choose_chunk(p->n, tau, iters);
+    int64_t chunk = schunk;
     if (R > 0) chunk = std::min(chunk, R);
-    auto chunk_len = [&](int64_t done) {
-        int64_t c = std::min(chunk, iters - done);
-        if (R > 0) c = std::min(c, R - (done % R));
-        return c;
-    };
+    auto chunk_len = [&](int64_t done) { return std::min(schunk, iters - done); };
     SamplerPlan sp;
-    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, chunk, &sp,
+    if ((s = sampler_workspace(&p->samp_mem, &p->samp_cap, p->n, tau, schunk, &sp,
                                spec.kind == PCDM_SAMPLING_INDEPENDENT)) != PCDM_OK)
         return s;
     SamplingDev sdev;
@@ -1018,42 +1017,51 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
 
     if (presample) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
-    // iterations per launch of the iteration kernel: up to 64 (PCDM_ITER_CHUNK), each
-    // launch's slots drawn in sampler chunks of `chunk` iterations; fewer launches of the
-    // persistent kernel (each costs its ramp-up and drain)
+    // iterations per launch of the iteration kernel: max(schunk, 64) (PCDM_ITER_CHUNK for
+    // the 64; each launch of the persistent kernel costs its ramp-up and drain), never
+    // across a residual refresh.  Slots are drawn ahead in windows of max(schunk, ichunk)
+    // iterations (one sampler pass can cover several refresh periods: tiny, medium),
+    // each window in sampler passes of schunk iterations.
     int64_t ichunk = chunk;
     if (!batched) {
         int64_t want = 64;
         if (const char* ic = getenv("PCDM_ITER_CHUNK")) want = std::max<int64_t>(1, atoll(ic));
-        ichunk = std::max(chunk, std::min(want, iters));
+        ichunk = std::max(schunk, std::min(want, iters));  // long launches when samples are cheap
         if (R > 0) ichunk = std::min(ichunk, R);
+        ichunk = std::max<int64_t>(ichunk, 1);
     }
-    const bool own_slots = !presample && ichunk > chunk;
-    if (own_slots && p->slot_cap < (size_t)(ichunk * tau)) {
+    const int64_t win = std::min(iters, std::max(schunk, ichunk));
+    const bool own_slots = !presample && win > schunk;
+    if (own_slots && p->slot_cap < (size_t)(win * tau)) {
         cudaFree(p->slot_buf);
         p->slot_buf = nullptr;
         p->slot_cap = 0;
-        CK(cudaMalloc((void**)&p->slot_buf, sizeof(int) * ichunk * tau), "alloc slot buffer");
-        p->slot_cap = (size_t)(ichunk * tau);
+        CK(cudaMalloc((void**)&p->slot_buf, sizeof(int) * win * tau), "alloc slot buffer");
+        p->slot_cap = (size_t)(win * tau);
     }
+    int* const win_slots = own_slots ? p->slot_buf : sp.slots;
+    int64_t w0 = 0, w1 = 0;  // sampled window [w0, w1) of run-local iterations
     auto iter_len = [&](int64_t done) {
         int64_t c = std::min(ichunk, iters - done);
         if (R > 0) c = std::min(c, R - (done % R));
+        if (!presample) c = std::min(c, w1 - done);
         return c;
     };
     bool list_restarted = false;
     int64_t done = 0;
     while (done < iters) {
-        const int64_t c = iter_len(done);
-        int* slots_c = presample ? p->pre_slots + done * tau : (own_slots ? p->slot_buf : sp.slots);
         int ts;
         CK(tm.begin(&ts), "event");
-        if (!presample) {
-            for (int64_t s0 = 0; s0 < c; s0 += chunk)
-                CK(sample_chunk(sp.w, sdev, seed, first_iter + done + s0, std::min(chunk, c - s0), slots_c + s0 * tau,
-                                &p->sc->flags, st, p->sms, &launches),
+        if (!presample && done >= w1) {
+            w0 = done;
+            w1 = std::min(iters, done + win);
+            for (int64_t s0 = w0; s0 < w1; s0 += schunk)
+                CK(sample_chunk(sp.w, sdev, seed, first_iter + s0, std::min(schunk, w1 - s0),
+                                win_slots + (s0 - w0) * tau, &p->sc->flags, st, p->sms, &launches),
                    "sampler");
         }
+        const int64_t c = iter_len(done);
+        int* slots_c = presample ? p->pre_slots + done * tau : win_slots + (done - w0) * tau;
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
         CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed || batched ? 0 : 3 * sizeof(int)), st),
