@@ -44,7 +44,7 @@ cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, d
                               const DevCSR* csr = nullptr);
 cudaError_t build_csr(const DevCSC& A, const int* counts, DevCSR* out, cudaStream_t st, int sms, int64_t* launches);
 cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,
-                           int64_t* launches);
+                           int64_t* launches, float* r2 = nullptr, int* zero = nullptr, int nzero = 0);
 cudaError_t launch_objective_sums(int64_t m, int64_t n, const double* r64, const float* x, double* out,
                                   cudaStream_t st, int sms, int64_t* launches);
 

@@ -211,10 +211,17 @@ __global__ void scatter_x_kernel(int64_t n, const long long* __restrict__ colptr
     if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, bad);
 }
 
-__global__ void round_r_kernel(int64_t m, const double* __restrict__ r64, float* __restrict__ r) {
+// r = (float) r64; also into r2 (the one-barrier loop's second buffer) and zeroes
+// zero[0 .. nzero) when given
+__global__ void round_r_kernel(int64_t m, const double* __restrict__ r64, float* __restrict__ r,
+                               float* __restrict__ r2, int* __restrict__ zero, int nzero) {
+    if (zero && blockIdx.x == 0 && threadIdx.x < nzero) zero[threadIdx.x] = 0;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
-         t += (int64_t)gridDim.x * blockDim.x)
-        r[t] = (float)r64[t];
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const float v = (float)r64[t];
+        r[t] = v;
+        if (r2) r2[t] = v;
+    }
 }
 
 // out[0] += sum r64^2 ; out[1] += sum |x|
@@ -438,8 +445,8 @@ cudaError_t build_csr(const DevCSC& A, const int* counts, DevCSR* out, cudaStrea
 }
 
 cudaError_t launch_round_r(int64_t m, const double* r64, float* r, cudaStream_t st, int sms,
-                           int64_t* launches) {
-    round_r_kernel<<<grid_for(m, kThreads, sms * 8), kThreads, 0, st>>>(m, r64, r);
+                           int64_t* launches, float* r2, int* zero, int nzero) {
+    round_r_kernel<<<grid_for(m, kThreads, sms * 8), kThreads, 0, st>>>(m, r64, r, r2, zero, nzero);
     ++*launches;
     return cudaGetLastError();
 }

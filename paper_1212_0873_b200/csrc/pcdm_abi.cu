@@ -193,12 +193,14 @@ pcdm_status read_scalars(pcdm_problem* p, Scalars* host, cudaStream_t st) {
 }
 
 // r <- A x - b with fp64 accumulation (x device pointer).
+// r2 / zero: the rounding pass also fills the one-barrier loop's second buffer and
+// clears its step-list counters
 pcdm_status residual_from(pcdm_problem* p, const float* x, cudaStream_t st, int64_t* launches,
-                          const XHeaders* xh = nullptr) {
+                          const XHeaders* xh = nullptr, float* r2 = nullptr, int* zero = nullptr, int nzero = 0) {
     CK(launch_residual64(p->csc(), p->b, x, p->r64, &p->sc->flags, st, p->sms, launches, xh,
                          p->has_csr ? &p->csr : nullptr),
        "residual kernels");
-    CK(launch_round_r(p->m, p->r64, p->r, st, p->sms, launches), "residual rounding");
+    CK(launch_round_r(p->m, p->r64, p->r, st, p->sms, launches, r2, zero, nzero), "residual rounding");
     return PCDM_OK;
 }
 
@@ -863,8 +865,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
         xh = XHeaders{p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff};
     }
-    if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr)) != PCDM_OK) return s;
-    if (one_barrier) CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
+    if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr, one_barrier ? p->r2 : nullptr)) != PCDM_OK)
+        return s;
     CK(tm.end(T_SETUP, t0), "event");
     if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
     if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
@@ -1095,23 +1097,23 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         if (R > 0 && done % R == 0) {
             int tr;
             CK(tm.begin(&tr), "event");
-            if ((s = x_out()) != PCDM_OK) return s;  // the refresh reads x
+            float* r2 = one_barrier ? p->r2 : nullptr;
+            int* zero = one_barrier ? p->sc->nz_count : nullptr;
             if (xhdr) {
-                // restart the dirty list from the support of x (the refresh pass re-lists the
-                // nonzero x_i), so it does not grow with every step of a long run; the host
-                // copy-back then cannot name entries that became zero: it copies all of x
+                // the refresh reads x: headers -> x, and the dirty list restarts from the
+                // support of x (the refresh pass re-lists the nonzero x_i), so it does not
+                // grow with every step of a long run; the host copy-back then cannot name
+                // entries that became zero: it copies all of x
+                // (two passes: the list may name a column twice)
+                if ((s = x_out()) != PCDM_OK) return s;
                 CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff, p->n, st, p->sms,
                                      &launches),
                    "x headers");
                 CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
                 list_restarted = true;
-                if ((s = residual_from(p, xd, st, &launches, &xh)) != PCDM_OK) return s;
-            } else if ((s = residual_from(p, xd, st, &launches)) != PCDM_OK) {
+                if ((s = residual_from(p, xd, st, &launches, &xh, r2, zero, 3)) != PCDM_OK) return s;
+            } else if ((s = residual_from(p, xd, st, &launches, nullptr, r2, zero, 3)) != PCDM_OK) {
                 return s;
-            }
-            if (one_barrier) {
-                CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st), "copy r");
-                CK(cudaMemsetAsync(p->sc->nz_count, 0, 3 * sizeof(int), st), "memset lists");
             }
             CK(tm.end(T_SETUP, tr), "event");
             ++stats.refreshes;
