@@ -138,8 +138,9 @@ __device__ __forceinline__ uint64_t sampler_word(uint64_t seed, uint32_t k, uint
 
 // tau-independent (R16): processor j picks the first
 // accepted draw of counters (j, k, rho, tag 3); the lowest j keeps a shared pick.
+// (CAS-first insert; the entry index is recorded in `at` for the check pass, as in round 0)
 __global__ void sample_indep_insert_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables,
-                                           int* slots) {
+                                           int* slots, int* at) {
     const int64_t total = count * a.cnt;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -149,18 +150,18 @@ __global__ void sample_indep_insert_kernel(DrawArgs a, int64_t k0, int64_t count
         uint32_t rho = 0;
         while ((v = draw_value(a.seed, (uint32_t)(k0 + it), rho, j, 3u, a.n, a.reject_below)) < 0) ++rho;
         slots[t] = (int)v;
-        table_insert(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
+        at[t] = (int)table_insert_cas_first(tables + (it << a.log2h), a.log2h, (uint32_t)v, j);
     }
 }
 
-__global__ void sample_indep_check_kernel(DrawArgs a, int64_t count, const unsigned long long* tables, int* slots) {
+__global__ void sample_indep_check_kernel(DrawArgs a, int64_t count, const unsigned long long* tables, int* slots,
+                                          const int* at) {
     const int64_t total = count * a.cnt;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t it = t / a.cnt;
         const uint32_t j = (uint32_t)(t - it * a.cnt);
-        const int v = slots[t];
-        if (table_owner(tables + (it << a.log2h), a.log2h, (uint32_t)v) != j) slots[t] = -1;
+        if ((uint32_t)__ldcg(tables + (it << a.log2h) + at[t]) != j) slots[t] = -1;
     }
 }
 
@@ -294,8 +295,9 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
     if (sd.kind == 1) {  // tau-independent: one ownership pass, no redraws of collisions
         e = cudaMemsetAsync(w.tables, 0xFF, (size_t)count * ((size_t)1 << w.log2h) * 8, st);
         if (e != cudaSuccess) return e;
-        sample_indep_insert_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, slots);
-        sample_indep_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, slots);
+        // entry indices in the (otherwise unused) pending area: count * cnt ints
+        sample_indep_insert_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, slots, w.pending);
+        sample_indep_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, slots, w.pending);
         *launches += 2;
         return cudaGetLastError();
     }
