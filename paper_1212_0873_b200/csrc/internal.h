@@ -141,6 +141,7 @@ struct PackedParams {
     int64_t xlist_cap;
     const int* hot_rows;  // [nhot] ascending row ids of the hot rows (block row field 0x80000000 | h)
     int nhot;             // 0: no hot rows (blocks hold plain row ids)
+    int pipeline;         // 1: the next slot's block is loaded before the current slot's gathers
     int cluster_sync;     // 1 / 2: the grid is one thread-block cluster of 512- / 1024-thread CTAs,
                           //        the barriers are barrier.cluster
     int list_cap;         // > 0: nonzero steps staged per CTA in shared memory (capacity), one

@@ -159,26 +159,46 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? 3 : 1) pcdm_packed_kern
         }
 
         // ---------------- phase A: one coalesced block load + <= 2 gathers per lane
+        // Software pipeline over this group's slots: the next slot's id and block are
+        // loaded before the current slot's gathers.  The first slot was loaded before
+        // the previous barrier (S_k and A do not depend on r), so only its x_i, which a
+        // step of iteration k-1 may have changed, is read again; later blocks are loaded
+        // inside iteration k, after that barrier, and no other slot of iteration k changes
+        // their column (the slots of one iteration are distinct).
+        // (P.pipeline = 0, for DRAM-bound r: each block is loaded when its slot comes up)
+        // x_i lives in the block header (chunk 0 .z) when P.xlist: the column's single line
+        // brings it, no separate random x line; the header is then mutable, so the block is
+        // read through L2 (ld.cg) instead of the non-coherent path
+        auto load_block = [&](int col) {
+            return P.xlist ? ld_l2_v4(P.blocks + (int64_t)col * G + t) : ld_stream_v4(P.blocks + (int64_t)col * G + t);
+        };
+        const bool pipeline = P.pipeline != 0;
+        int i_nx = -1;
+        int4 c_nx = c_pf;
         for (int64_t j = gid; j < tau; j += ngroups) {
+            const bool first = j == gid;
             int i;
             int4 c;
-            float xi = 0.0f;
-            if (j == gid) {
-                // this group's first slot was loaded before the previous barrier (S_k and
-                // the block do not depend on r); only x_i, which a step of iteration k-1
-                // may have changed, is read again
+            if (first) {
                 i = i_pf;
                 c = c_pf;
-                if (i < 0) continue;
-                if (t == 0) xi = P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : ld_l2_f32(P.x + i);
+            } else if (pipeline) {
+                i = i_nx;
+                c = c_nx;
             } else {
                 i = ld_stream_s32(S + j);
-                if (i < 0) continue;  // idle processor (non-nice samplings)
-                // x_i lives in the block header (chunk 0 .z) when P.xlist: the column's single
-                // line brings it, no separate random x line; the header is then mutable, so
-                // the block is read through L2 (ld.cg) instead of the non-coherent path
-                c = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i * G + t) : ld_stream_v4(P.blocks + (int64_t)i * G + t);
-                if (t == 0) xi = P.xlist ? __int_as_float(c.z) : ld_l2_f32(P.x + i);
+                if (i >= 0) c = load_block(i);
+            }
+            const int64_t jn = j + ngroups;
+            if (pipeline && jn < tau) {
+                i_nx = ld_stream_s32(S + jn);
+                if (i_nx >= 0) c_nx = load_block(i_nx);
+            }
+            if (i < 0) continue;  // idle processor (non-nice samplings)
+            float xi = 0.0f;
+            if (t == 0) {
+                if (!P.xlist) xi = ld_l2_f32(P.x + i);
+                else xi = first ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : __int_as_float(c.z);
             }
             const int len = __shfl_sync(gm, c.y, src);
             float acc = 0.0f;

@@ -918,6 +918,15 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.hot_rows = p->hot_rows;
     Q.nhot = p->nhot;
     Q.list_cap = list_cap;
+    // software-pipelined slots when r is L2-resident (the loop is latency-bound there:
+    // large 26.1 -> 25.8, skewed tau=2^16 163 -> 158 ms/step); for r much larger than L2
+    // (huge) the extra loads in flight cost more than they hide (29.0 -> 29.4 ms)
+    {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
+        Q.pipeline = (double)p->m * 4.0 <= 0.5 * (double)l2;
+        if (const char* pl = getenv("PCDM_PIPELINE")) Q.pipeline = atoi(pl) != 0;
+    }
     // a grid that fits one cluster (<= 16 CTAs: small tau) synchronises with the hardware
     // cluster barrier instead of the global-memory grid barrier
     Q.cluster_sync = packed && plan.ctas <= 16 ? cluster_sync : 0;

@@ -428,3 +428,16 @@ def test_staged_step_list_and_dense_x(gpu, monkeypatch, stage, dense):
     xo = oracle.run(m, to_host(c), to_host(r), to_host(v), to_host(b), 0.0, 512, 30, 1).x
     assert np.max(np.abs(xh - xo)) <= 1e-4 * np.max(np.abs(xo))
     prob.close()
+
+
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+def test_packed_slot_pipeline_on_and_off(gpu, monkeypatch, pipeline):
+    # the software-pipelined slot loop (next block loaded before the current gathers) is
+    # chosen for L2-resident r; both forms against the oracle, several slots per group
+    monkeypatch.setenv("PCDM_PIPELINE", pipeline)
+    m, n = 6000, 40_000
+    c, r, v, b, lam = _ragged(m, n, np.random.default_rng(2).integers(0, 14, size=n), 23, lam_frac=0.05)
+    x0 = np.random.default_rng(6).normal(size=n) * (np.arange(n) % 9 == 0)
+    for tau, iters, refresh in ((40_000, 6, 3), (20_000, 12, 0), (999, 80, 0)):
+        out = run_both(c, r, v, b, lam, m, tau, iters, seed=tau, variant="packed", x0=x0, refresh_every=refresh)
+        assert_parity(out)

@@ -1,0 +1,12 @@
+# conditional slot pipelining: tests + configs
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/pytest_gpu.log
+bash tools/gpu_configs.sh > gpurun_out/configs_run.log 2>&1; echo "configs rc=$?"
+python - <<'PY'
+import json
+for l in open('gpurun_out/configs.jsonl'):
+    d=json.loads(l); print(d['config']['workload'], d['config']['tau'], '%.4g'%d['value'], round(d['ms_per_step'],2), d['variant'], d['breakdown_ms_per_step'])
+PY
