@@ -295,7 +295,9 @@ int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
     // keep one chunk's sampler tables + slots within ~40 MB so the sampler's random
     // atomics stay in L2 (126 MB) instead of going to HBM
     const size_t per = sampler_bytes_per_iter(n, tau, nullptr) + (size_t)tau * 4;
-    size_t budget = (size_t)64 << 20;
+    // 128 MB per sampler pass: huge 5.90 -> 5.17 ms/step of sampler, large 6.87 -> 5.54
+    // (profiles/r01_sampler_mb_ab.jsonl; 256 MB is no better)
+    size_t budget = (size_t)128 << 20;
     if (const char* mb = getenv("PCDM_SAMPLER_MB")) budget = (size_t)std::max(1, atoi(mb)) << 20;
     int64_t c = (int64_t)std::max<size_t>(1, budget / per);
     c = std::min<int64_t>(c, 8192);
