@@ -292,8 +292,8 @@ pcdm_status sampler_workspace(void** mem, size_t* cap, int64_t n, int64_t tau, i
 }
 
 int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
-    // keep one chunk's sampler tables + slots within ~40 MB so the sampler's random
-    // atomics stay in L2 (126 MB) instead of going to HBM
+    // one sampler pass's tables + slots within a budget: large enough that the per-pass
+    // launches amortise, small enough that the random atomics mostly stay in L2
     const size_t per = sampler_bytes_per_iter(n, tau, nullptr) + (size_t)tau * 4;
     // 128 MB per sampler pass: huge 5.90 -> 5.17 ms/step of sampler, large 6.87 -> 5.54
     // (profiles/r01_sampler_mb_ab.jsonl; 256 MB is no better)
