@@ -37,16 +37,57 @@ struct DrawArgs {
     int log2h;
 };
 
+// Contest mode (round 0 without a check pass): a draw that finds its value already in
+// the table is a duplicate; it records (entry, its code, the code it found) in the
+// iteration's contest list (second half of the pending area, cnt/3 records) and lowers
+// the entry to the minimum code; a rejected draw goes straight to the pending list.  The
+// rounds kernel then knows every slot that drew a contested value: the one that wrote
+// the entry first appears as a found code (the first duplicate's CAS reads it before
+// any atomicMin), all others as recording codes.  Too many records for the list: the
+// iteration's counter passes cnt/3 and the rounds kernel checks all its slots.
+__device__ __forceinline__ void contest_record(int* pending, int* ncontest, int64_t it, int64_t cnt, uint32_t h,
+                                               uint32_t code, uint32_t found) {
+    const int cap = (int)(cnt / 3);
+    const int q = atomicAdd(ncontest + it, 1);
+    if (q < cap) {
+        int* rec = pending + it * 2 * cnt + cnt + 3 * q;
+        rec[0] = (int)h;
+        rec[1] = (int)code;
+        rec[2] = (int)found;
+    }
+}
+
 template <bool CAS_FIRST>
 __global__ void sample_round0_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables,
-                                     int* cand, int* pending) {
+                                     int* cand, int* pending, int* npending, int contest) {
     const int64_t total = count * a.cnt;
+    const uint32_t mask = (1u << a.log2h) - 1u;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t it = t / a.cnt;
         const uint32_t j = (uint32_t)(t - it * a.cnt);
         const long long v = draw_value(a.seed, (uint32_t)(k0 + it), 0u, j, a.tag, a.n, a.reject_below);
         cand[t] = (int)v;
+        if (CAS_FIRST && contest) {
+            if (v < 0) {
+                pending[it * 2 * a.cnt + atomicAdd(npending + it, 1)] = (int)j;
+                continue;
+            }
+            unsigned long long* table = tables + (it << a.log2h);
+            const unsigned long long key = ((unsigned long long)v << 32) | j;
+            uint32_t h = hash_slot((uint32_t)v, a.log2h);
+            while (true) {
+                const unsigned long long prev = atomicCAS(&table[h], PCDM_EMPTY_SLOT, key);
+                if (prev == PCDM_EMPTY_SLOT) break;
+                if ((uint32_t)(prev >> 32) == (uint32_t)v) {
+                    atomicMin(&table[h], key);
+                    contest_record(pending, npending + count, it, a.cnt, h, j, (uint32_t)prev);
+                    break;
+                }
+                h = (h + 1) & mask;
+            }
+            continue;
+        }
         if (v >= 0) {
             if (CAS_FIRST) {
                 // the entry index goes to the (still unused) second half of the iteration's
@@ -81,16 +122,43 @@ __global__ void sample_check_kernel(DrawArgs a, int64_t count, const unsigned lo
 }
 
 // One CTA per iteration finishes rounds rho >= 1 for its pending slots.
-__global__ void sample_rounds_kernel(DrawArgs a, int64_t k0, unsigned long long* tables, int* cand,
-                                     int* pending, const int* npending, int* rounds_max, int* flags) {
+__global__ void sample_rounds_kernel(DrawArgs a, int64_t k0, int64_t count, unsigned long long* tables, int* cand,
+                                     int* pending, const int* npending, int* rounds_max, int* flags, int contest) {
     const int64_t it = blockIdx.x;
-    int np = npending[it];
-    if (np == 0) return;
     unsigned long long* table = tables + (it << a.log2h);
     int* c = cand + it * a.cnt;
     int* pin = pending + it * 2 * a.cnt;
     int* pout = pin + a.cnt;
     __shared__ int s_next;
+    int np = npending[it];
+    if (contest) {
+        // the losers of round 0: from the contest records, or (list overflow) every slot
+        const int nrec = npending[count + it];
+        if (nrec == 0 && np == 0) return;
+        if (threadIdx.x == 0) s_next = np;
+        __syncthreads();
+        auto lose = [&](uint32_t code) {  // append once (mark the slot's value -2)
+            if (atomicExch(c + code, -2) != -2) pin[atomicAdd(&s_next, 1)] = (int)code;
+        };
+        if (nrec > (int)(a.cnt / 3)) {
+            for (int t = threadIdx.x; t < a.cnt; t += blockDim.x) {
+                const int v = c[t];
+                if (v >= 0 && table_owner(table, a.log2h, (uint32_t)v) != (uint32_t)t) lose((uint32_t)t);
+            }
+        } else {
+            const int* rec = pin + a.cnt;
+            for (int q = threadIdx.x; q < nrec; q += blockDim.x) {
+                const uint32_t owner = (uint32_t)__ldcg(table + rec[3 * q]);
+                const uint32_t code = (uint32_t)rec[3 * q + 1], found = (uint32_t)rec[3 * q + 2];
+                if (code != owner) lose(code);
+                if (found != owner) lose(found);
+            }
+        }
+        __syncthreads();
+        np = s_next;
+        __syncthreads();
+    }
+    if (np == 0) return;
     uint32_t rho = 1;
     for (; np > 0; ++rho) {
         if ((uint64_t)(rho + 1) * (uint64_t)a.cnt > 0x100000000ull) {
@@ -305,7 +373,7 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
     if (w.cnt > 0) {
         e = cudaMemsetAsync(w.tables, 0xFF, (size_t)count * ((size_t)1 << w.log2h) * 8, st);
         if (e != cudaSuccess) return e;
-        e = cudaMemsetAsync(w.npending, 0, (size_t)count * sizeof(int), st);
+        e = cudaMemsetAsync(w.npending, 0, (size_t)count * 2 * sizeof(int), st);  // + contest counters
         if (e != cudaSuccess) return e;
         // CAS straight on the home entry (the tables were just cleared): huge sampler
         // 8.23 -> 7.05 ms/step, large 8.80 -> 7.68 (profiles/r01_sampler_cas_first_ab.jsonl);
@@ -321,18 +389,29 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
             const char* v = getenv("PCDM_CHECK_AT");
             return !(v && atoi(v) == 0);
         }();
+        // contest mode (default with CAS-first): duplicates recorded at insert time, no
+        // check pass over all slots (PCDM_CONTEST=0: check pass)
+        static const bool contest = [] {
+            const char* v = getenv("PCDM_CONTEST");
+            return !(v && atoi(v) == 0);
+        }();
+        const int cm = cas_first && contest ? 1 : 0;
         if (cas_first) {
-            sample_round0_kernel<true><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand, rec_at ? w.pending : nullptr);
+            sample_round0_kernel<true><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand,
+                                                               (rec_at || cm) ? w.pending : nullptr, w.npending, cm);
         } else {
-            sample_round0_kernel<false><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand, nullptr);
+            sample_round0_kernel<false><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand, nullptr, w.npending, 0);
         }
-        if (cas_first && rec_at)
-            sample_check_kernel<true><<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
-        else
-            sample_check_kernel<false><<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
-        sample_rounds_kernel<<<(unsigned)count, 1024, 0, st>>>(a, k0, w.tables, cand, w.pending, w.npending,
-                                                               w.rounds_max, flags);
-        *launches += 3;
+        if (!cm) {
+            if (cas_first && rec_at)
+                sample_check_kernel<true><<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
+            else
+                sample_check_kernel<false><<<blocks, 256, 0, st>>>(a, count, w.tables, cand, w.pending, w.npending);
+            ++*launches;
+        }
+        sample_rounds_kernel<<<(unsigned)count, 1024, 0, st>>>(a, k0, count, w.tables, cand, w.pending, w.npending,
+                                                               w.rounds_max, flags, cm);
+        *launches += 2;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

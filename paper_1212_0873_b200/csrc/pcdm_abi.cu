@@ -264,7 +264,7 @@ pcdm_status sampler_workspace(void** mem, size_t* cap, int64_t n, int64_t tau, i
     const size_t o_slots = off; off += al((size_t)chunk * tau * 4);
     const size_t o_cand = off; off += comp ? al((size_t)chunk * cnt * 4) : 0;
     const size_t o_pend = off; off += al((size_t)chunk * 2 * (cnt ? cnt : 1) * 4);
-    const size_t o_np = off; off += al((size_t)chunk * 4);
+    const size_t o_np = off; off += al((size_t)chunk * 8);  // npending[chunk] + ncontest[chunk]
     const size_t o_marks = off; off += comp ? al((size_t)chunk * n) : 0;
     const size_t o_rmax = off; off += 256;
     if (off > *cap) {
