@@ -91,8 +91,11 @@ __device__ __forceinline__ float gather_r(const float* rP, int v, const float* s
     return cache ? s_hot[v & 0x7fffffff] : ld_l2_f32(rP + s_hrow[v & 0x7fffffff]);
 }
 
+#ifndef PCDM_PACKED_MINB
+#define PCDM_PACKED_MINB 3  // CTAs of 512 threads per SM (register cap 40)
+#endif
 template <int G, bool ONE_BARRIER, bool LOGISTIC, int TPB = kThreads>
-__global__ void __launch_bounds__(TPB, TPB == kThreads ? 3 : 1) pcdm_packed_kernel(PackedParams P) {
+__global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) pcdm_packed_kernel(PackedParams P) {
     const int t = threadIdx.x & (G - 1);  // lane within the column group
     const unsigned gm = gmask_of<G>();
     const int src = (threadIdx.x & 31) & ~(G - 1);
