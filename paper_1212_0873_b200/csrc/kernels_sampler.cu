@@ -397,7 +397,21 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
         }();
         const int cm = cas_first && contest ? 1 : 0;
         if (cas_first) {
-            sample_round0_kernel<true><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand,
+            // round 0 in 128-thread blocks, up to 8 waves of them: fewer draws per thread and
+            // block-level load balance for the CAS round trips (huge sampler 4.0 -> 3.5 ms/step,
+            // profiles/r01_sampler_r0_shape_ab.jsonl; PCDM_R0_TPB / PCDM_R0_WAVES for A/B)
+            static const int r0_tpb = [] {
+                const char* v = getenv("PCDM_R0_TPB");
+                const int x = v ? atoi(v) : 128;
+                return (x == 64 || x == 128 || x == 256 || x == 512 || x == 1024) ? x : 128;
+            }();
+            static const int r0_waves = [] {
+                const char* v = getenv("PCDM_R0_WAVES");
+                const int x = v ? atoi(v) : 8;
+                return x >= 1 && x <= 64 ? x : 8;
+            }();
+            const int r0_blocks = blocks_for(count * w.cnt, r0_tpb, sms * (2048 / r0_tpb) * r0_waves);
+            sample_round0_kernel<true><<<r0_blocks, r0_tpb, 0, st>>>(a, k0, count, w.tables, cand,
                                                                (rec_at || cm) ? w.pending : nullptr, w.npending, cm);
         } else {
             sample_round0_kernel<false><<<blocks, 256, 0, st>>>(a, k0, count, w.tables, cand, nullptr, w.npending, 0);
