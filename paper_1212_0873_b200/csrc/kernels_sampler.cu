@@ -363,8 +363,10 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
     if (sd.kind == 1) {  // tau-independent: one ownership pass, no redraws of collisions
         e = cudaMemsetAsync(w.tables, 0xFF, (size_t)count * ((size_t)1 << w.log2h) * 8, st);
         if (e != cudaSuccess) return e;
-        // entry indices in the (otherwise unused) pending area: count * cnt ints
-        sample_indep_insert_kernel<<<blocks, 256, 0, st>>>(a, k0, count, w.tables, slots, w.pending);
+        // entry indices in the (otherwise unused) pending area: count * cnt ints; the insert
+        // pass in 128-thread blocks, up to 8 waves (as round 0 of the tau-nice sampler)
+        const int ib = blocks_for(count * w.cnt, 128, sms * 16 * 8);
+        sample_indep_insert_kernel<<<ib, 128, 0, st>>>(a, k0, count, w.tables, slots, w.pending);
         sample_indep_check_kernel<<<blocks, 256, 0, st>>>(a, count, w.tables, slots, w.pending);
         *launches += 2;
         return cudaGetLastError();
