@@ -109,6 +109,11 @@ struct IterParams {
     unsigned long long* nz_total;  // accumulates #delta != 0
     int64_t m, n;
     int logistic;         // 1: L2-regularised logistic loss (margins in r)
+    // shared-memory variant: residual refreshes inside the kernel (r = fp32(Ax - b),
+    // fp64 accumulation) after every run-local iteration k with (k + 1) % R == 0
+    const float* b;
+    int64_t k0;           // run-local index of this launch's first iteration
+    int64_t R;            // refresh period (0: none)
 };
 
 struct IterLaunch {

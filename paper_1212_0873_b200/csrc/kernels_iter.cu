@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
     float* s_r = s_x + n;                        // m
     int* s_nzi = (int*)(s_r + m);                // tau
     float* s_nzd = (float*)(s_nzi + tau);        // tau
+    double* s_r64 = (double*)(((uintptr_t)(s_nzd + tau) + 7) & ~(uintptr_t)7);  // m (refresh scratch)
     __shared__ int s_cnt;
 
     for (int t = threadIdx.x; t <= n; t += blockDim.x) s_col[t] = (int)P.colptr[t];
@@ -196,6 +197,21 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
         __syncthreads();
         if (threadIdx.x == 0) s_cnt = 0;
         __syncthreads();
+        if (P.R > 0 && (P.k0 + it + 1) % P.R == 0) {
+            // residual refresh (R8): r = fp32(A x - b) with fp64 accumulation, as the
+            // host-side refresh of the other variants
+            for (int t = threadIdx.x; t < m; t += blockDim.x) s_r64[t] = -(double)P.b[t];
+            __syncthreads();
+            for (int i = gid; i < n; i += ngroups) {
+                const double xi = (double)s_x[i];
+                if (xi == 0.0) continue;
+                for (int q = s_col[i] + lane_g; q < s_col[i + 1]; q += G)
+                    atomicAdd(s_r64 + s_row[q], (double)s_val[q] * xi);
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < m; t += blockDim.x) s_r[t] = (float)s_r64[t];
+            __syncthreads();
+        }
     }
     for (int t = threadIdx.x; t < n; t += blockDim.x) P.x[t] = s_x[t];
     for (int t = threadIdx.x; t < m; t += blockDim.x) P.r[t] = s_r[t];
@@ -203,7 +219,8 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
 }
 
 size_t smem_bytes(int64_t m, int64_t n, int64_t nnz, int64_t tau) {
-    return (size_t)(n + 1) * 4 + (size_t)nnz * 8 + (size_t)n * 8 + (size_t)m * 4 + (size_t)tau * 8;
+    return (size_t)(n + 1) * 4 + (size_t)nnz * 8 + (size_t)n * 8 + (size_t)m * 4 + (size_t)tau * 8 + 8 +
+           (size_t)m * 8;  // + the refresh scratch
 }
 
 int pow2_clamp(int64_t v, int lo, int hi) {

@@ -1054,9 +1054,13 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
     int* const win_slots = own_slots ? p->slot_buf : sp.slots;
     int64_t w0 = 0, w1 = 0;  // sampled window [w0, w1) of run-local iterations
+    // the shared-memory variant refreshes the residual inside the kernel: its launches
+    // are not cut at refresh points
+    const bool kernel_refresh = !packed && !batched && !clustered && plan.variant == PCDM_VARIANT_SMEM;
+    if (kernel_refresh) ichunk = std::max(ichunk, std::min<int64_t>(iters, std::max<int64_t>(schunk, 1)));
     auto iter_len = [&](int64_t done) {
         int64_t c = std::min(ichunk, iters - done);
-        if (R > 0) c = std::min(c, R - (done % R));
+        if (R > 0 && !kernel_refresh) c = std::min(c, R - (done % R));
         if (!presample) c = std::min(c, w1 - done);
         return c;
     };
@@ -1100,12 +1104,16 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         } else {
             P.slots = slots_c;
             P.iters = c;
+            P.k0 = done;
+            P.R = kernel_refresh ? R : 0;
+            P.b = p->b;
             CK(launch_iter(plan, P, st, &launches), "iteration kernel");
         }
         CK(tm.end(T_ITER, ti), "event");
         ++stats.iter_launches;
         done += c;
-        if (R > 0 && done % R == 0) {
+        if (kernel_refresh && R > 0) stats.refreshes += (done / R) - ((done - c) / R);
+        if (R > 0 && done % R == 0 && !kernel_refresh) {
             int tr;
             CK(tm.begin(&tr), "event");
             float* r2 = one_barrier ? p->r2 : nullptr;

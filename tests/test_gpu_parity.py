@@ -187,10 +187,13 @@ def test_host_and_device_x_agree(gpu):
 
 
 @pytest.mark.parametrize("refresh", [-1, 1, 7])
-def test_refresh_cadence(gpu, refresh):
+@pytest.mark.parametrize("variant", ["grid", "smem"])
+def test_refresh_cadence(gpu, refresh, variant):
+    # (the shared-memory variant refreshes inside its kernel, the others between launches)
     c, r, v, b, lam = _ragged(500, 400, np.full(400, 5), 6)
-    out = run_both(c, r, v, b, lam, 500, 40, 100, seed=4, refresh_every=refresh, variant="grid")
+    out = run_both(c, r, v, b, lam, 500, 40, 100, seed=4, refresh_every=refresh, variant=variant)
     assert_parity(out)
+    assert out["stats"]["refreshes"] == (0 if refresh < 0 else 100 // refresh)
     # maintained residual vs the oracle's (and vs Ax-b of the oracle's x)
     np.testing.assert_allclose(out["r_gpu"], out["res"].r, rtol=0, atol=1e-4 * np.max(np.abs(out["res"].r)))
 
