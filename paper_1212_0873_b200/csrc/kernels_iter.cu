@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
     int* s_nzi = (int*)(s_r + m);                // tau
     float* s_nzd = (float*)(s_nzi + tau);        // tau
     double* s_r64 = (double*)(((uintptr_t)(s_nzd + tau) + 7) & ~(uintptr_t)7);  // m (refresh scratch)
-    __shared__ int s_cnt;
+    __shared__ int s_cnt2[2];  // step counter, double-buffered (no reset barrier)
 
     for (int t = threadIdx.x; t <= n; t += blockDim.x) s_col[t] = (int)P.colptr[t];
     for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
         s_x[t] = P.x[t];
     }
     for (int t = threadIdx.x; t < m; t += blockDim.x) s_r[t] = P.r[t];
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x < 2) s_cnt2[threadIdx.x] = 0;
     __syncthreads();
 
     const int lane_g = threadIdx.x & (G - 1);
@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
 
     for (int64_t it = 0; it < P.iters; ++it) {
         const int* S = P.slots + it * tau;
+        int* s_cnt = s_cnt2 + (it & 1);
         for (int j = gid; j < tau; j += ngroups) {
             const int i = S[j];
             if (i < 0) continue;  // idle processor
@@ -180,22 +181,22 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
                 if (d != 0.0f) {
                     if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
                     s_x[i] = xp;
-                    const int pos = atomicAdd(&s_cnt, 1);
+                    const int pos = atomicAdd(s_cnt, 1);
                     s_nzi[pos] = i;
                     s_nzd[pos] = d;
                 }
             }
         }
         __syncthreads();
-        const int cnt = s_cnt;
+        const int cnt = *s_cnt;
         for (int t = gid; t < cnt; t += ngroups) {
             const int i = s_nzi[t];
             const float d = s_nzd[t];
             for (int q = s_col[i] + lane_g; q < s_col[i + 1]; q += G) atomicAdd(s_r + s_row[q], s_val[q] * d);
         }
         nz_total += (unsigned long long)cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) s_cnt = 0;
+        if (threadIdx.x == 0) s_cnt2[(it + 1) & 1] = 0;  // the next iteration's counter (read last
+                                                          // in iteration it-1, before the barrier above)
         __syncthreads();
         if (P.R > 0 && (P.k0 + it + 1) % P.R == 0) {
             // residual refresh (R8): r = fp32(A x - b) with fp64 accumulation, as the
