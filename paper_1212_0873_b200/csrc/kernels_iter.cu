@@ -18,6 +18,7 @@
 //   SMEM  one CTA, colptr/rowidx/val/L/x/r copied into shared memory.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <stdint.h>
@@ -303,6 +304,7 @@ IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau
     if (variant == 2) {
         L.ctas = 1;
         L.lanes = pow2_clamp(avg, 1, 32);
+        if (const char* sl = getenv("PCDM_SMEM_LANES")) L.lanes = pow2_clamp(atoi(sl), 1, 32);  // A/B
         // as many threads as the slots need (each __syncthreads waits for all of them)
         L.threads = std::max(64, std::min(kSmemThreads, pow2_clamp(tau * L.lanes, 64, kSmemThreads)));
         L.smem = sm;
