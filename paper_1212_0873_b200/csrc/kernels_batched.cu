@@ -34,6 +34,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -378,6 +379,135 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_kernel(BatchedParams
     }
 }
 
+// Pass 3 with one thread per slot (G <= 8: the slot record is G/2 16-byte vectors,
+// <= 14 rows).  Same arithmetic as pcdm_batched_kernel; a thread tests its slot's
+// rows against the filter alone, so no group shuffles, and its first slot's record
+// is loaded before the filter update so the two latencies overlap.  A Bloom hit or a
+// nonzero step reads the column's block in the thread (rare on LASSO).
+template <int G, bool LOGISTIC>
+__global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedParams P) {
+    static_assert(G >= 2 && G <= 8, "one slot record per thread");
+    constexpr int NV = G / 2;
+    const int t = threadIdx.x & (G - 1);
+    const unsigned gm = gmask_of<G>();
+    const int src = (threadIdx.x & 31) & ~(G - 1);
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int grp = threadIdx.x / G;
+    const int pair0 = 2 * (t - 1);
+    const int64_t tau = P.tau;
+    extern __shared__ unsigned s_bf[];
+    unsigned* s_cf = s_bf + (1 << (kBloomLog - 5));
+    int* s_hrow = (int*)(s_cf + (1 << (kColLog - 5)));
+    for (int w = threadIdx.x; w < (1 << (kBloomLog - 5)) + (1 << (kColLog - 5)); w += blockDim.x) s_bf[w] = 0u;
+    for (int h = threadIdx.x; h < P.nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
+    unsigned bar_target = 0;
+    __syncthreads();
+
+    for (int64_t it = 0; it < P.iters; ++it) {
+        const float* DP = (it & 1) ? P.d1 : P.d0;
+        float* DQ = (it & 1) ? P.d0 : P.d1;
+        const int4* rec = (const int4*)(P.rec + it * tau * G);
+        const int* S = P.slots + it * tau;
+        const float* g0 = P.g0 + it * tau;
+        // this thread's first slot, in flight across the filter update
+        int ipf = -1;
+        int4 rpf[NV];
+        float gpf = 0.0f;
+        if (tid < tau) {
+            ipf = ld_stream_s32(S + tid);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rpf[v] = ld_stream_v4(rec + tid * NV + v);
+            gpf = __ldcg(g0 + tid);
+        }
+        if (it > 0) {
+            const int cntp = ld_l2_s32(P.nz_count + it - 1);
+            const int* lidx = P.nz_idx + (it - 1) * tau;
+            for (int e = grp; e < cntp; e += kThreads / G) {
+                const int i = ld_l2_s32(lidx + e);
+                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int len = __shfl_sync(gm, c.y, src);
+                if (t == 0) bloom_set<kColLog>(s_cf, (uint32_t)i);
+                if (t > 0 && pair0 < len) bloom_set<kBloomLog>(s_bf, (uint32_t)real_row(c.x, s_hrow));
+                if (t > 0 && pair0 + 1 < len) bloom_set<kBloomLog>(s_bf, (uint32_t)real_row(c.z, s_hrow));
+            }
+            for (int64_t e = gid; e < cntp; e += ngroups) {
+                const int i = ld_l2_s32(lidx + e);
+                const float d = ld_l2_f32(P.nz_delta + (it - 1) * tau + e);
+                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int len = __shfl_sync(gm, c.y, src);
+                if (t > 0 && pair0 < len) red_add_f32(DQ + real_row(c.x, s_hrow), __int_as_float(c.y) * d);
+                if (t > 0 && pair0 + 1 < len) red_add_f32(DQ + real_row(c.z, s_hrow), __int_as_float(c.w) * d);
+            }
+            __syncthreads();
+        }
+        auto process = [&](int64_t j, int i, const int4* rv, float acc) {
+            const int4* blk = P.blocks + (int64_t)i * G;
+            bool hit = false;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                if (v > 0) {
+                    hit |= rv[v].x >= 0 && bloom_test<kBloomLog>(s_bf, (uint32_t)rv[v].x);
+                    hit |= rv[v].y >= 0 && bloom_test<kBloomLog>(s_bf, (uint32_t)rv[v].y);
+                }
+                hit |= rv[v].z >= 0 && bloom_test<kBloomLog>(s_bf, (uint32_t)rv[v].z);
+                hit |= rv[v].w >= 0 && bloom_test<kBloomLog>(s_bf, (uint32_t)rv[v].w);
+            }
+            int len = -1;
+            if (hit) {
+                len = ld_l2_v4(blk).y;
+#pragma unroll
+                for (int l = 1; l < G; ++l) {
+                    const int4 c = ld_l2_v4(blk + l);
+                    if (2 * (l - 1) < len) acc += dirty_term<LOGISTIC>(P, DP, s_bf, real_row(c.x, s_hrow), __int_as_float(c.y));
+                    if (2 * (l - 1) + 1 < len)
+                        acc += dirty_term<LOGISTIC>(P, DP, s_bf, real_row(c.z, s_hrow), __int_as_float(c.w));
+                }
+            }
+            float xi;
+            if (!P.xlist) xi = ld_l2_f32(P.x + i);
+            else if (bloom_test<kColLog>(s_cf, (uint32_t)i)) xi = ld_l2_f32((const float*)blk + 2);
+            else xi = __int_as_float(rv[0].y);
+            const float xp = block_step<LOGISTIC>(xi, acc, P.beta * __int_as_float(rv[0].x), P.lambda);
+            const float d = xp - xi;
+            if (d == 0.0f) return;
+            if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
+            if (P.xlist) {
+                ((float*)blk)[2] = xp;
+                if (P.xlist_cap > 0) {
+                    const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
+                    if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = i;
+                }
+            } else {
+                P.x[i] = xp;
+            }
+            const int pos = atomicAdd(P.nz_count + it, 1);
+            P.nz_idx[it * tau + pos] = i;
+            P.nz_delta[it * tau + pos] = d;
+            if (len < 0) len = ld_stream_v4(blk).y;
+#pragma unroll
+            for (int l = 1; l < G; ++l) {
+                if (2 * (l - 1) >= len) break;
+                const int4 c = ld_stream_v4(blk + l);
+                red_add_f32(DQ + real_row(c.x, s_hrow), __int_as_float(c.y) * d);
+                if (2 * (l - 1) + 1 < len) red_add_f32(DQ + real_row(c.z, s_hrow), __int_as_float(c.w) * d);
+            }
+        };
+        if (ipf >= 0) process(tid, ipf, rpf, gpf);
+        for (int64_t j = tid + nth; j < tau; j += nth) {
+            const int i = ld_stream_s32(S + j);
+            if (i < 0) continue;
+            int4 rv[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rv[v] = ld_stream_v4(rec + j * NV + v);
+            process(j, i, rv, __ldcg(g0 + j));
+        }
+        if (it + 1 < P.iters) grid_barrier(P.barrier, bar_target);
+    }
+}
+
 // ---------------------------------------------------------------- fold
 // r += sum of the chunk's steps (a_i delta_i), D0 = D1 = 0 on their rows.
 template <int G>
@@ -414,6 +544,21 @@ __global__ void batch_fold_kernel(BatchedParams P) {
     if (nz) atomicAdd(P.nz_total, nz);
 }
 
+// pass 3: one thread per slot for G <= 8 (PCDM_BATCHED_GROUP=1: one group per slot)
+template <int G>
+const void* step_kernel(bool logistic) {
+    if constexpr (G <= 8) {
+        static const bool group = [] {
+            const char* v = getenv("PCDM_BATCHED_GROUP");
+            return v && atoi(v) != 0;
+        }();
+        if (!group)
+            return logistic ? (const void*)pcdm_batched_slot_kernel<G, true>
+                            : (const void*)pcdm_batched_slot_kernel<G, false>;
+    }
+    return logistic ? (const void*)pcdm_batched_kernel<G, true> : (const void*)pcdm_batched_kernel<G, false>;
+}
+
 template <int G>
 size_t expand_smem(int cq_log, int nb) {
     const size_t ne = (size_t)1 << cq_log;
@@ -437,19 +582,13 @@ cudaError_t launch_all(const BatchedParams& P, int ctas3, cudaStream_t st, int s
         batch_sweep_kernel<false><<<sms * 4, kThreads, 0, st>>>(P);
     void* args[] = {(void*)&P};
     const size_t sm3 = batched_step_smem(P.nhot);
-    e = cudaLaunchCooperativeKernel(P.logistic ? (const void*)pcdm_batched_kernel<G, true>
-                                               : (const void*)pcdm_batched_kernel<G, false>,
-                                    dim3(ctas3), dim3(kThreads), args, sm3, st);
+    e = cudaLaunchCooperativeKernel(step_kernel<G>(P.logistic), dim3(ctas3), dim3(kThreads), args, sm3, st);
     if (e != cudaSuccess) return e;
     batch_fold_kernel<G><<<sms * 4, kThreads, 0, st>>>(P);
     *launches += 4;
     return cudaGetLastError();
 }
 
-template <int G>
-const void* step_kernel(bool logistic) {
-    return logistic ? (const void*)pcdm_batched_kernel<G, true> : (const void*)pcdm_batched_kernel<G, false>;
-}
 
 }  // namespace
 
