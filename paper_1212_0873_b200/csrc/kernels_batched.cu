@@ -45,8 +45,14 @@ using namespace pcdm_internal;
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kBloomLog = 18;  // dirty-row filter: 2^18 bits = 32 KB of shared memory per CTA
-constexpr int kColLog = 15;    // stepped-column filter: 2^15 bits = 4 KB
+constexpr int kBloomLog = 19;  // dirty-row filter: 2^19 bits = 64 KB of shared memory per CTA
+constexpr int kColLog = 16;    // stepped-column filter: 2^16 bits = 8 KB
+#ifndef PCDM_BATCHED_UP
+#define PCDM_BATCHED_UP 1  // pass 3: slots per thread loaded before the filter update
+#endif
+#ifndef PCDM_EXPAND_MINB
+#define PCDM_EXPAND_MINB 2
+#endif
 
 __device__ __forceinline__ int4 ld_l2_v4(const int4* p) {
     int4 v;
@@ -81,25 +87,30 @@ __device__ __forceinline__ unsigned gmask_of() {
 // real row of a block entry (hot rows are stored as 0x80000000 | h, kernels_packed.cu)
 __device__ __forceinline__ int real_row(int v, const int* hrow) { return v < 0 ? hrow[v & 0x7fffffff] : v; }
 
-// one-hash Bloom filters (bit arrays of 2^LOG bits): a false positive costs one block
-// read, a miss is impossible
+// two-hash Bloom filters (bit arrays of 2^LOG bits): a false positive costs one block
+// read, a miss is impossible.  With k rows set, a row tests positive with probability
+// ~(2k / 2^LOG)^2 (huge, k ~ 3000 per chunk: ~1.4e-4, against 6e-3 for one hash on
+// 2^18 bits; one hit stalls the whole warp on the serial block read of pass 3)
 template <int LOG>
-__device__ __forceinline__ uint32_t bloom_h(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - LOG); }
+__device__ __forceinline__ uint32_t bloom_h1(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - LOG); }
+template <int LOG>
+__device__ __forceinline__ uint32_t bloom_h2(uint32_t v) { return ((v ^ (v >> 15)) * 0x2C1B3C6Du) >> (32 - LOG); }
 template <int LOG>
 __device__ __forceinline__ void bloom_set(unsigned* bf, uint32_t v) {
-    const uint32_t a = bloom_h<LOG>(v);
+    const uint32_t a = bloom_h1<LOG>(v), b = bloom_h2<LOG>(v);
     atomicOr(bf + (a >> 5), 1u << (a & 31));
+    atomicOr(bf + (b >> 5), 1u << (b & 31));
 }
 template <int LOG>
 __device__ __forceinline__ bool bloom_test(const unsigned* bf, uint32_t v) {
-    const uint32_t a = bloom_h<LOG>(v);
-    return (bf[a >> 5] >> (a & 31)) & 1u;
+    const uint32_t a = bloom_h1<LOG>(v), b = bloom_h2<LOG>(v);
+    return (bf[a >> 5] >> (a & 31)) & (bf[b >> 5] >> (b & 31)) & 1u;
 }
 
 // ---------------------------------------------------------------- pass 1: expand + sort
 // Dynamic shared memory: stage int2[cq*maxe] | inv u16[cq*maxe] | cnt int[nb] | cur int[nb+1]
 template <int G>
-__global__ void __launch_bounds__(kThreads, 2) batch_expand_kernel(BatchedParams P) {
+__global__ void __launch_bounds__(kThreads, PCDM_EXPAND_MINB) batch_expand_kernel(BatchedParams P) {
     constexpr int MAXE = 2 * (G - 1);
     extern __shared__ int4 s_raw[];
     const int cq = 1 << P.cq_log;
@@ -412,15 +423,21 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
         const int4* rec = (const int4*)(P.rec + it * tau * G);
         const int* S = P.slots + it * tau;
         const float* g0 = P.g0 + it * tau;
-        // this thread's first slot, in flight across the filter update
-        int ipf = -1;
-        int4 rpf[NV];
-        float gpf = 0.0f;
-        if (tid < tau) {
-            ipf = ld_stream_s32(S + tid);
+        // this thread's first UP slots, in flight across the filter update
+        constexpr int UP = PCDM_BATCHED_UP;
+        int ipf[UP];
+        int4 rpf[UP][NV];
+        float gpf[UP];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) rpf[v] = ld_stream_v4(rec + tid * NV + v);
-            gpf = __ldcg(g0 + tid);
+        for (int u = 0; u < UP; ++u) {
+            const int64_t j = tid + u * nth;
+            ipf[u] = -1;
+            if (j < tau) {
+                ipf[u] = ld_stream_s32(S + j);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) rpf[u][v] = ld_stream_v4(rec + j * NV + v);
+                gpf[u] = __ldcg(g0 + j);
+            }
         }
         if (it > 0) {
             const int cntp = ld_l2_s32(P.nz_count + it - 1);
@@ -495,8 +512,10 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
                 if (2 * (l - 1) + 1 < len) red_add_f32(DQ + real_row(c.z, s_hrow), __int_as_float(c.w) * d);
             }
         };
-        if (ipf >= 0) process(tid, ipf, rpf, gpf);
-        for (int64_t j = tid + nth; j < tau; j += nth) {
+#pragma unroll
+        for (int u = 0; u < UP; ++u)
+            if (ipf[u] >= 0) process(tid + u * nth, ipf[u], rpf[u], gpf[u]);
+        for (int64_t j = tid + UP * nth; j < tau; j += nth) {
             const int i = ld_stream_s32(S + j);
             if (i < 0) continue;
             int4 rv[NV];

@@ -941,7 +941,14 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
 
     BatchedParams B{};
     int bat_ctas = 0;
+    // BATCHED: iterations per snapshot (the passes' unit), at most one refresh period
+    int64_t bchunk = chunk;
+    if (const char* bc = getenv("PCDM_BATCHED_CHUNK")) {
+        bchunk = std::min<int64_t>(std::max<int64_t>(1, atoll(bc)), std::max<int64_t>(iters, 1));
+        if (R > 0) bchunk = std::min(bchunk, R);
+    }
     if (batched) {
+        const int64_t chunk = bchunk;
         const int G = p->packed_G;
         B.cq_log = batched_cq_log(G);
         B.rb = batched_rb(B.cq_log);
@@ -1035,7 +1042,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // across a residual refresh.  Slots are drawn ahead in windows of max(schunk, ichunk)
     // iterations (one sampler pass can cover several refresh periods: tiny, medium),
     // each window in sampler passes of schunk iterations.
-    int64_t ichunk = chunk;
+    int64_t ichunk = batched ? bchunk : chunk;
     if (!batched) {
         int64_t want = 64;
         if (const char* ic = getenv("PCDM_ITER_CHUNK")) want = std::max<int64_t>(1, atoll(ic));
