@@ -41,7 +41,7 @@ METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
 VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", 6: "cluster", -1: "async"}
 KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
-                     5: "batch_expand+batch_sweep+pcdm_batched+batch_fold", 6: "pcdm_cluster_kernel",
+                     5: "batch_expand+batch_sweep+pcdm_batched_slot+batch_fold", 6: "pcdm_cluster_kernel",
                      -1: "pcdm_async_kernel"}
 # oracle iterations per reference step / cpu_baseline sample, per config
 REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4, "logistic_small": 200, "kddb_like": 4}
@@ -202,12 +202,13 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config, iters_per_launch):
-    """DRAM bytes per iteration-kernel launch from the committed ncu capture, if any."""
+def ncu_traffic(config, variant, iters_per_launch):
+    """DRAM bytes per iteration-kernel launch from the committed ncu capture of this
+    config and loop ("<config>:<variant>"), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)[config]
+            d = json.load(f)["%s:%s" % (config, variant)]
         return float(d["dram_bytes_per_iter"]) * iters_per_launch
     except Exception:
         return None
@@ -388,7 +389,8 @@ def bench_ours(args, world, rank, local):
     launch_ms = it_ms / max(it_launches, 1)
     achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
     peak, peak_src = hbm_peak()
-    traffic = None if args.async_ else ncu_traffic(cfg.name, iters_per_launch)
+    traffic = None if args.async_ else ncu_traffic(cfg.name, VARIANT_NAMES.get(st_list[-1]["variant"], "?"),
+                                                    iters_per_launch)
     launches = sum(s["kernel_launches"] for s in st_list)
     nz = sum(s["nonzero_deltas"] for s in st_list)
 

@@ -110,6 +110,9 @@ struct pcdm_problem {
     size_t pre_cap = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+    // AUTO BATCHED guard: the nonzero-step count, read back without stalling the stream
+    unsigned long long* nz_host = nullptr;
+    cudaEvent_t ev_nz = nullptr;
     Scalars* sc = nullptr;     // device scalars
     // per-run workspaces (grown on demand)
     int* nz_idx = nullptr;
@@ -167,6 +170,8 @@ void free_problem(pcdm_problem* p) {
         cudaEventDestroy(p->ev_s0);
         cudaEventDestroy(p->ev_s1);
     }
+    if (p->ev_nz) cudaEventDestroy(p->ev_nz);
+    cudaFreeHost(p->nz_host);
     cudaFree(p->sc);
     cudaFree(p->nz_idx);
     cudaFree(p->nz_delta);
@@ -741,14 +746,24 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // AUTO: packed blocks whenever the shared-memory variant does not apply
     bool packed = p->packed_G > 0 &&
                   (variant >= PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
-    // BATCHED (kernels_batched.cu): on request only, for now
-    bool batched = packed && (variant == PCDM_VARIANT_BATCHED ||
-                              (variant == PCDM_VARIANT_AUTO && getenv("PCDM_BATCHED") && atoi(getenv("PCDM_BATCHED")) != 0));
-    if (batched) packed = false;
+    // BATCHED (kernels_batched.cu): AUTO picks it for LASSO when r is much larger than L2
+    // (huge: 3.90e9 -> 4.60e9 updates/s; large, skewed, kddb_like stay on the packed loop,
+    // profiles/r01_batched_vs_packed.txt), with the packed loop prepared as a fallback
+    // should the run's steps turn out too dense for its filters (below).  PCDM_BATCHED=0/1
+    // overrides the size rule.
+    int l2_bytes = 0;
+    cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, p->device);
+    const char* bat_env = getenv("PCDM_BATCHED");
+    const bool auto_batched =
+        variant == PCDM_VARIANT_AUTO &&
+        (bat_env ? atoi(bat_env) != 0 : p->loss == 0 && p->packed_G <= 8 && (double)p->m * 4.0 > 2.0 * l2_bytes);
+    bool batched = packed && (variant == PCDM_VARIANT_BATCHED || auto_batched);
+    const bool bat_fallback = batched && variant == PCDM_VARIANT_AUTO;
+    if (batched && !bat_fallback) packed = false;
     // CLUSTER (kernels_cluster.cu): r in one cluster's distributed shared memory
     int cl_size = 0, cl_rpc = 0, cl_cap = 0;
     size_t cl_smem = 0;
-    if (packed && (variant == PCDM_VARIANT_CLUSTER || variant == PCDM_VARIANT_AUTO)) {
+    if (packed && !batched && (variant == PCDM_VARIANT_CLUSTER || variant == PCDM_VARIANT_AUTO)) {
         // AUTO only with PCDM_CLUSTER=1: measured slower than the grid loop on medium
         // (5.0 vs 3.8 us per iteration, profiles/r01_cluster_medium_ab.jsonl)
         const char* ce = getenv("PCDM_CLUSTER");
@@ -829,6 +844,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                 list_cap = (int)cap;
         }
     }
+    const IterLaunch packed_plan = plan;  // the AUTO BATCHED fallback
+    if (batched) packed = false;
     if (p->nz_cap < tau) {
         cudaFree(p->nz_idx);
         cudaFree(p->nz_delta);
@@ -867,7 +884,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
         xh = XHeaders{p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff};
     }
-    if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr, one_barrier ? p->r2 : nullptr)) != PCDM_OK)
+    if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr, one_barrier && !batched ? p->r2 : nullptr)) !=
+        PCDM_OK)
         return s;
     CK(tm.end(T_SETUP, t0), "event");
     if ((s = read_scalars(p, &hs, st)) != PCDM_OK) return s;
@@ -931,7 +949,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
     // a grid that fits one cluster (<= 16 CTAs: small tau) synchronises with the hardware
     // cluster barrier instead of the global-memory grid barrier
-    Q.cluster_sync = packed && plan.ctas <= 16 ? cluster_sync : 0;
+    Q.cluster_sync = (packed || bat_fallback) && packed_plan.ctas <= 16 ? cluster_sync : 0;
     // cache the hot rows when the hottest one is read >= 1024 times per iteration
     // (tau count_max / n); below that the per-iteration copy costs more than the
     // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;
@@ -1072,8 +1090,41 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         return c;
     };
     bool list_restarted = false;
+    // AUTO BATCHED guard: after each batched launch the nonzero-step count is copied to
+    // pinned host memory behind an event; when a completed copy shows more dirty rows per
+    // snapshot than the filters hold (kBloomLog = 19: ~16 K rows keep a false positive
+    // below ~0.5 %), the rest of the run goes to the packed loop (r2 = r, empty step lists:
+    // the state it starts from after a refresh)
+    int64_t nz_at = 0;  // run-local iterations the last issued copy covers
+    bool nz_pending = false;
+    if (bat_fallback && !p->nz_host) {
+        CK(cudaMallocHost((void**)&p->nz_host, sizeof(unsigned long long)), "alloc pinned counter");
+        CK(cudaEventCreateWithFlags(&p->ev_nz, cudaEventDisableTiming), "event");
+    }
+    const double avg_len = p->n > 0 ? (double)p->nnz / (double)p->n : 0.0;
     int64_t done = 0;
     while (done < iters) {
+        if (batched && bat_fallback && nz_pending) {
+            static const bool sync_check = getenv("PCDM_BATCHED_SYNC_CHECK") != nullptr;  // tests: deterministic
+            const cudaError_t q = sync_check ? cudaEventSynchronize(p->ev_nz) : cudaEventQuery(p->ev_nz);
+            if (q == cudaSuccess) {
+                nz_pending = false;
+                const double rows_per_chunk =
+                    (double)*p->nz_host / (double)std::max<int64_t>(nz_at, 1) * (double)bchunk * avg_len;
+                if (rows_per_chunk > 16384.0 || getenv("PCDM_BATCHED_FORCE_FALLBACK")) {
+                    batched = false;
+                    packed = true;
+                    plan = packed_plan;
+                    if (one_barrier) CK(cudaMemcpyAsync(p->r2, p->r, sizeof(float) * p->m, cudaMemcpyDeviceToDevice, st),
+                                        "copy residual");
+                    CK(cudaMemsetAsync(p->sc->nz_count, 0, 3 * sizeof(int), st), "memset step lists");
+                }
+            } else if (q != cudaErrorNotReady) {
+                CK(q, "event query");
+            } else {
+                cudaGetLastError();  // not-ready is not an error
+            }
+        }
         int ts;
         CK(tm.begin(&ts), "event");
         if (!presample && done >= w1) {
@@ -1103,6 +1154,13 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             B.iters = c;
             B.nq = (int)((c * tau + (1ll << B.cq_log) - 1) >> B.cq_log);
             CK(launch_batched(p->packed_G, B, bat_ctas, st, p->sms, &launches), "batched iteration kernels");
+            if (bat_fallback && !nz_pending) {
+                CK(cudaMemcpyAsync(p->nz_host, &p->sc->nz_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
+                   "read step count");
+                CK(cudaEventRecord(p->ev_nz, st), "event");
+                nz_at = done + c;
+                nz_pending = true;
+            }
         } else if (packed) {
             Q.slots = slots_c;
             Q.iters = c;
@@ -1145,7 +1203,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             ++stats.refreshes;
         }
     }
-    p->r_cur = (one_barrier && (iters & 1)) ? p->r2 : p->r;
+    p->r_cur = (one_barrier && !batched && (iters & 1)) ? p->r2 : p->r;
     int tx;
     CK(tm.begin(&tx), "event");
     if ((s = x_out()) != PCDM_OK) return s;

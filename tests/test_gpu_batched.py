@@ -111,3 +111,50 @@ def test_batched_logistic(gpu):
     for tau, lam in ((37, 1.0), (400, 0.1)):
         check(run_both_logistic(colptr, rowidx, val, y, lam, m, tau, 80, seed=tau, variant="batched", x0=x0,
                                 first_iter=3))
+
+
+def _auto_batched(monkeypatch, chunk="5"):
+    # the size rule (r > 2 x L2) off: PCDM_BATCHED=1 makes AUTO take the batched loop with
+    # its packed fallback on any size; the guard reads the step count synchronously
+    monkeypatch.setenv("PCDM_BATCHED", "1")
+    monkeypatch.setenv("PCDM_BATCHED_SYNC_CHECK", "1")
+    monkeypatch.setenv("PCDM_BATCHED_CHUNK", chunk)
+
+
+def test_auto_batched_falls_back_on_dense_steps(gpu, monkeypatch):
+    # small lambda and a dense start: most steps nonzero, more dirty rows per snapshot than
+    # the filters hold -> the packed loop takes over after the first snapshot (at an odd
+    # iteration: the one-barrier loop starts from r2 = r and empty step lists)
+    _auto_batched(monkeypatch)
+    inst = I.generate(I.InstanceConfig("dense_steps", 200_000, 20_000, 10, 20_000, lam_frac=0.001), seed=2)
+    x0 = np.random.default_rng(4).normal(size=inst.n)
+    for tau, iters, refresh in ((4000, 23, 0), (4000, 40, 12), (20_000, 9, -1)):
+        out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, tau, iters, seed=tau, x0=x0,
+                       refresh_every=refresh)
+        assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
+        assert out["stats"]["iter_launches"] >= 2
+        assert_parity(out)
+        _check_r(out)
+
+
+def test_auto_batched_keeps_sparse_steps(gpu, monkeypatch):
+    # large lambda from x = 0: few nonzero steps, the batched loop runs the whole run
+    _auto_batched(monkeypatch)
+    inst = I.generate(I.InstanceConfig("sparse_steps", 200_000, 20_000, 10, 100, lam_frac=0.5), seed=3)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 2000, 37, seed=3)
+    assert out["stats"]["variant"] == pcdm.VARIANTS["batched"]
+    assert_parity(out)
+    _check_r(out)
+
+
+@pytest.mark.parametrize("chunk", ["4", "7"])
+def test_auto_batched_forced_fallback(gpu, monkeypatch, chunk):
+    # the hand-off itself on a multi-bin instance, at an even and an odd iteration
+    _auto_batched(monkeypatch, chunk)
+    monkeypatch.setenv("PCDM_BATCHED_FORCE_FALLBACK", "1")
+    inst = I.generate(I.InstanceConfig("bins", 5_000_000, 300_000, 10, 3000, lam_frac=0.01), seed=1)
+    x0 = np.random.default_rng(2).normal(size=inst.n) * (np.arange(inst.n) % 50 == 0)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 4096, 30, seed=7, x0=x0)
+    assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
+    assert_parity(out)
+    _check_r(out)

@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full `huge` size (m = 1e8, n = 5e8, 5e9 nonzeros), in
-the launch configuration bench.py times (AUTO -> the packed loop, tau = 2^18).
+the launch configuration bench.py times (AUTO -> the batched loop, tau = 2^18), and
+for the packed loop.
 
 The oracle cannot hold the whole run, but the first K iterations only ever touch
 the columns S_0 .. S_{K-1} draw, and with x_0 = 0 every other column stays zero:
@@ -64,32 +65,35 @@ def test_huge_full_size_first_iterations(gpu):
     np.testing.assert_allclose(Lh, (vals ** 2).sum(1).astype(np.float32), rtol=2e-7, atol=0)
     del L
 
-    x = torch.zeros(inst.n, dtype=torch.float32, device=gpu)
-    prob.run(x, tau, K, seed=seed)
-    st = prob.stats()
-    assert st["variant"] == pcdm.VARIANTS["packed"] and st["iters"] == K
-    F_gpu = prob.objective(x)
+    # AUTO (the batched loop: r is 400 MB, much larger than L2) and the packed loop
+    runs = {}
+    for variant, want in (("auto", "batched"), ("packed", "packed")):
+        x = torch.zeros(inst.n, dtype=torch.float32, device=gpu)
+        prob.run(x, tau, K, seed=seed, variant=variant)
+        st = prob.stats()
+        assert st["variant"] == pcdm.VARIANTS[want] and st["iters"] == K
+        r_gpu = torch.empty(inst.m, dtype=torch.float32, device=gpu)
+        prob.residual(r_gpu)
+        runs[want] = (prob.objective(x), to_host(x), to_host(r_gpu))
+        del x, r_gpu
     beta = prob.beta(tau)  # from the full matrix's omega (the sub-matrix's omega is smaller)
     assert abs(beta - oracle.beta(prob.omega, tau, inst.n)) <= 1e-15 * beta
-    r_gpu = torch.empty(inst.m, dtype=torch.float32, device=gpu)
-    prob.residual(r_gpu)
-    r_gpu = to_host(r_gpu)
     prob.close()
 
     cols, colptr, rows, vals = _subinstance(inst, tau, K, seed)
     b, lam, m = to_host(inst.b), inst.lam, inst.m
-    xg = to_host(x)
-    del inst, x
+    del inst
     torch.cuda.empty_cache()
     res = oracle.run(m, colptr, rows, vals, b, lam, tau, K, seed, beta_override=beta)
     F_orc = oracle.objective(m, colptr, rows, vals, b, lam, res.x)
-    assert abs(F_gpu - F_orc) <= F_RTOL * abs(F_orc), (F_gpu, F_orc)
-    # x: zero off the touched columns, oracle values on them
-    untouched = np.ones(xg.size, dtype=bool)
+    untouched = np.ones(runs["packed"][1].size, dtype=bool)
     untouched[cols] = False
-    assert not np.any(xg[untouched])
     xo = res.x[cols]
     scale = max(np.max(np.abs(xo)), 1e-30)
-    assert np.max(np.abs(xg[cols].astype(np.float64) - xo)) <= X_RTOL * scale
-    # the maintained residual over all 1e8 rows
-    assert np.max(np.abs(r_gpu - res.r)) <= 1e-4 * np.max(np.abs(res.r))
+    for name, (F_gpu, xg, r_gpu) in runs.items():
+        assert abs(F_gpu - F_orc) <= F_RTOL * abs(F_orc), (name, F_gpu, F_orc)
+        # x: zero off the touched columns, oracle values on them
+        assert not np.any(xg[untouched]), name
+        assert np.max(np.abs(xg[cols].astype(np.float64) - xo)) <= X_RTOL * scale, name
+        # the maintained residual over all 1e8 rows
+        assert np.max(np.abs(r_gpu - res.r)) <= 1e-4 * np.max(np.abs(res.r)), name
