@@ -52,6 +52,9 @@ constexpr int kSweepMaxQ = 40;  // pass 2: slot ranges per CTA (x 2 KB of shared
 #ifndef PCDM_SWEEP_HW
 #define PCDM_SWEEP_HW 16
 #endif
+#ifndef PCDM_EXPAND_U
+#define PCDM_EXPAND_U 4  // pass 1: slots per group in flight
+#endif
 #ifndef PCDM_BATCHED_UP
 #define PCDM_BATCHED_UP 1  // pass 3: slots per thread loaded before the filter update
 #endif
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, PCDM_EXPAND_MINB) batch_expand_kerne
         for (int b = threadIdx.x; b < P.nb; b += blockDim.x) cnt[b] = 0;
         __syncthreads();
         // U slots per group in flight: the slot ids, then their blocks, then the entries
-        constexpr int U = 4;
+        constexpr int U = PCDM_EXPAND_U;
         constexpr int GPC = kThreads / G;  // groups per CTA
         for (int sl0 = grp; sl0 < cq; sl0 += GPC * U) {
             int iv[U];
