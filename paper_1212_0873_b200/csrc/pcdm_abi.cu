@@ -754,9 +754,21 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     int l2_bytes = 0;
     cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, p->device);
     const char* bat_env = getenv("PCDM_BATCHED");
+    // ... and when an iteration samples enough columns to amortise the snapshot's
+    // per-iteration barrier and filter latency, with few idle slots (its passes cost per
+    // slot, active or not).  Huge (profiles/r01_batched_autorule_ab.txt): tau-nice 2^17,
+    // 1.5 2^17, 2^18, 2^19 and tau-independent 2^18 win by 14-23 %; (2^18, 0.75)-binomial
+    // ties, (2^18, 0.5)-binomial loses (2.63e9 vs 2.95e9 updates/s).  Rule: E|S| >= 2^17
+    // and E|S| >= 0.8 tau (PCDM_BATCHED_MIN_SLOTS overrides the first).
+    double es1 = 0.0, es2 = 0.0;
+    sampling_moments(spec, p->n, &es1, &es2);
+    double min_slots = 131072.0;
+    if (const char* ms = getenv("PCDM_BATCHED_MIN_SLOTS")) min_slots = atof(ms);
     const bool auto_batched =
         variant == PCDM_VARIANT_AUTO &&
-        (bat_env ? atoi(bat_env) != 0 : p->loss == 0 && p->packed_G <= 8 && (double)p->m * 4.0 > 2.0 * l2_bytes);
+        (bat_env ? atoi(bat_env) != 0
+                 : p->loss == 0 && p->packed_G <= 8 && (double)p->m * 4.0 > 2.0 * l2_bytes && es1 >= min_slots &&
+                       es1 >= 0.8 * (double)tau);
     bool batched = packed && (variant == PCDM_VARIANT_BATCHED || auto_batched);
     const bool bat_fallback = batched && variant == PCDM_VARIANT_AUTO;
     if (batched && !bat_fallback) packed = false;
