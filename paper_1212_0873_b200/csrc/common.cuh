@@ -67,18 +67,37 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // fences (-DPCDM_SC_BARRIER restores the __threadfence + atomicAdd form).  Work
 // issued between arrive and wait overlaps the other CTAs' arrival (it must not
 // write anything the barrier is meant to publish).
+// PCDM_BARRIER_SPLIT = K > 1: CTA b arrives on counter b % K (K counters 128 bytes
+// apart, so the arrivals do not serialise on one L2 address) and warp 0 polls all K.
+// The barrier memory is kBarrierWords words (zeroed before each launch).
+#ifndef PCDM_BARRIER_SPLIT
+#define PCDM_BARRIER_SPLIT 1
+#endif
+constexpr int kBarrierWords = 8 * 32;
+static_assert(PCDM_BARRIER_SPLIT >= 1 && PCDM_BARRIER_SPLIT <= 8, "at most 8 barrier counters");
 #ifndef PCDM_SC_BARRIER
 __device__ __forceinline__ void grid_arrive(unsigned* counter, unsigned& target) {
     __syncthreads();
     target += gridDim.x;
-    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+    if (threadIdx.x == 0) {
+        unsigned* c = counter + (PCDM_BARRIER_SPLIT > 1 ? (blockIdx.x % PCDM_BARRIER_SPLIT) * 32 : 0);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
+    }
 }
 __device__ __forceinline__ void grid_wait(const unsigned* counter, unsigned target) {
-    if (threadIdx.x == 0) {
-        while ((int)(ld_acquire_u32(counter) - target) < 0) {
+    if (PCDM_BARRIER_SPLIT == 1) {
+        if (threadIdx.x == 0) {
+            while ((int)(ld_acquire_u32(counter) - target) < 0) {
 #ifdef PCDM_BARRIER_SLEEP
-            __nanosleep(PCDM_BARRIER_SLEEP);
+                __nanosleep(PCDM_BARRIER_SLEEP);
 #endif
+            }
+        }
+    } else if (threadIdx.x < 32) {
+        const unsigned lane = threadIdx.x;
+        for (;;) {
+            const unsigned v = lane < PCDM_BARRIER_SPLIT ? ld_acquire_u32(counter + lane * 32) : 0u;
+            if ((int)(__reduce_add_sync(0xffffffffu, v) - target) >= 0) break;
         }
     }
     __syncthreads();

@@ -57,13 +57,13 @@ bool is_device_ptr(const void* p) {
 // Scalars living in one small device block.
 struct Scalars {
     int flags;
-    unsigned barrier;
     int nz_count[3];
     int max_out;
     int rounds_max;
     unsigned long long nz_total;
     unsigned long long mismatches;
     double sums[2];
+    alignas(128) unsigned barrier[pcdm::kBarrierWords];  // grid-barrier counter(s), common.cuh
 };
 
 }  // namespace
@@ -923,7 +923,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     P.nz_idx = p->nz_idx;
     P.nz_delta = p->nz_delta;
     P.nz_count = p->sc->nz_count;
-    P.barrier = &p->sc->barrier;
+    P.barrier = p->sc->barrier;
     P.flags = &p->sc->flags;
     P.nz_total = &p->sc->nz_total;
     P.m = p->m;
@@ -940,7 +940,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.nz_idx = p->nz_idx;
     Q.nz_delta = p->nz_delta;
     Q.nz_count = p->sc->nz_count;
-    Q.barrier = &p->sc->barrier;
+    Q.barrier = p->sc->barrier;
     Q.flags = &p->sc->flags;
     Q.nz_total = &p->sc->nz_total;
     Q.logistic = p->loss;
@@ -1024,7 +1024,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         B.nz_delta = (float*)(base + o_del);
         B.nz_count = (int*)(base + o_cnt);
         B.rec = (int2*)(base + o_rec);
-        B.barrier = &p->sc->barrier;
+        B.barrier = p->sc->barrier;
         B.flags = &p->sc->flags;
         B.nz_total = &p->sc->nz_total;
         B.x = xd;
@@ -1151,8 +1151,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         int* slots_c = presample ? p->pre_slots + done * tau : win_slots + (done - w0) * tau;
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
-        CK(cudaMemsetAsync(&p->sc->barrier, 0, sizeof(unsigned) + (packed || batched ? 0 : 3 * sizeof(int)), st),
-           "memset barrier");
+        CK(cudaMemsetAsync(p->sc->barrier, 0, sizeof(p->sc->barrier), st), "memset barrier");
+        if (!packed && !batched) CK(cudaMemsetAsync(p->sc->nz_count, 0, 3 * sizeof(int), st), "memset step lists");
         if (batched) CK(cudaMemsetAsync(B.nz_count, 0, sizeof(int) * c, st), "memset step lists");
         CK(tm.end(T_SAMPLER, ts), "event");
         int ti;
