@@ -58,7 +58,11 @@ typedef enum {
  * read phase (all g_i of S_k from r_k) and the write phase (r += delta_i a_i)
  * runs and where the data lives. */
 typedef enum {
-    PCDM_VARIANT_AUTO = 0, /* pick by problem size                                      */
+    PCDM_VARIANT_AUTO = 0, /* pick by problem size: SMEM when A fits shared memory;
+                             BATCHED for LASSO when 4m > 2 x L2 and E|S| >= 2^17 and
+                             E|S| >= 0.8 tau (handing the rest of the run to PACKED if
+                             its steps turn out dense); PACKED
+                             otherwise when max column length <= 62; GRID beyond    */
     PCDM_VARIANT_GRID = 1, /* persistent cooperative grid, r in HBM/L2, grid barriers    */
     PCDM_VARIANT_SMEM = 2, /* one CTA, A, r, x, L resident in shared memory (small A)    */
     PCDM_VARIANT_BLOCK = 3, /* one CTA, data in HBM/L2, __syncthreads barriers           */
@@ -71,7 +75,8 @@ typedef enum {
                                row bin, r streamed through L2 once per chunk), plus
                                a_i^T (r_k - r_0) on the rows the chunk's steps touched.
                                Same iteration (alg:PCD1), different summation order of g_i.
-                               For r much larger than L2.  Needs max column length <= 62 */
+                               For r much larger than L2 and sparse steps (LASSO).  Needs
+                               max column length <= 62 */
     PCDM_VARIANT_CLUSTER = 6 /* packed blocks; r split over the shared memories of one
                                thread-block cluster (<= 16 CTAs), gathers and scatters in
                                distributed shared memory, two hardware cluster barriers per
