@@ -205,7 +205,8 @@ struct BatchedParams {
     int2* gent;           // [nq][cq * maxe] sorted entries (row_local | slot_local << rb, val)
     int* offs;            // [nq][nb + 1] bin starts
     int nq, cq_log, nb, rb, maxe;
-    int2* rec;            // [iters * tau][G] slot records: lane 0 {L_i, x_i}, lane t real rows 2t-2, 2t-1 (-1: none)
+    int2* rec;            // [iters * tau][2 rnv] slot records: lane 0 {L_i, x_i}, lane t real rows 2t-2, 2t-1 (-1: none)
+    int rnv;              // 16-byte vectors per slot record: 1 + ceil((max column length - 2) / 4), <= G / 2
     int* nz_idx;          // [iters][tau] nonzero steps per iteration
     float* nz_delta;      // [iters][tau]
     int* nz_count;        // [iters], zeroed before the chunk

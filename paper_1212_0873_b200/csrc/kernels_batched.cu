@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(kThreads, PCDM_EXPAND_MINB) batch_expand_kerne
                 }
                 // the slot record of pass 3, 8 bytes per lane: lane 0 {L_i, x_i}, lane t the
                 // real rows of its two entries (-1 = none)
-                if (tt < total) P.rec[tt * G + t] = t == 0 ? make_int2(cv[u].x, cv[u].z) : make_int2(ea.x, eb.x);
+                if (tt < total && t < 2 * P.rnv)
+                    P.rec[tt * 2 * P.rnv + t] = t == 0 ? make_int2(cv[u].x, cv[u].z) : make_int2(ea.x, eb.x);
             }
         }
         __syncthreads();
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
     for (int64_t it = 0; it < P.iters; ++it) {
         const float* DP = (it & 1) ? P.d1 : P.d0;
         float* DQ = (it & 1) ? P.d0 : P.d1;
-        const int4* rec = (const int4*)(P.rec + it * tau * G);
+        const int4* rec = (const int4*)(P.rec + it * tau * 2 * P.rnv);
         const int* S = P.slots + it * tau;
         const float* g0 = P.g0 + it * tau;
         // this thread's first UP slots, in flight across the filter update
@@ -471,7 +472,8 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
             if (j < tau) {
                 ipf[u] = ld_stream_s32(S + j);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) rpf[u][v] = ld_stream_v4(rec + j * NV + v);
+                for (int v = 0; v < NV; ++v)
+                    rpf[u][v] = v < P.rnv ? ld_stream_v4(rec + j * P.rnv + v) : make_int4(-1, -1, -1, -1);
                 gpf[u] = __ldcg(g0 + j);
             }
         }
@@ -556,7 +558,8 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
             if (i < 0) continue;
             int4 rv[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) rv[v] = ld_stream_v4(rec + j * NV + v);
+            for (int v = 0; v < NV; ++v)
+                rv[v] = v < P.rnv ? ld_stream_v4(rec + j * P.rnv + v) : make_int4(-1, -1, -1, -1);
             process(j, i, rv, __ldcg(g0 + j));
         }
         if (it + 1 < P.iters) grid_barrier(P.barrier, bar_target);
@@ -622,8 +625,15 @@ size_t expand_smem(int cq_log, int nb) {
 }
 
 template <int G>
-cudaError_t launch_all(const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches) {
+cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int sms, int64_t* launches) {
     cudaError_t e;
+    // slot records: P.rnv 16-byte vectors (rows 2 + 4 (rnv - 1) >= max column length);
+    // the G-lane-group step kernel reads G / 2
+    BatchedParams P = P0;
+    if (step_kernel<G>(P.logistic) == (P.logistic ? (const void*)pcdm_batched_kernel<G, true>
+                                                  : (const void*)pcdm_batched_kernel<G, false>))
+        P.rnv = G / 2;
+    P.rnv = std::max(1, std::min(P.rnv, G / 2));
     const size_t sm1 = expand_smem<G>(P.cq_log, P.nb);
     e = cudaFuncSetAttribute(batch_expand_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     if (e != cudaSuccess) return e;

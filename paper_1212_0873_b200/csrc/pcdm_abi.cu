@@ -1024,6 +1024,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         B.nz_delta = (float*)(base + o_del);
         B.nz_count = (int*)(base + o_cnt);
         B.rec = (int2*)(base + o_rec);
+        B.rnv = 1 + (int)((std::max<int64_t>(p->max_len - 2, 0) + 3) / 4);  // 10 entries (huge): 3 vectors, 48 B
         B.barrier = p->sc->barrier;
         B.flags = &p->sc->flags;
         B.nz_total = &p->sc->nz_total;
