@@ -110,6 +110,7 @@ struct pcdm_problem {
     size_t pre_cap = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+    std::vector<cudaEvent_t> pass_ev;  // PCDM_PRESAMPLE_DEV: one event per presampler pass
     // AUTO BATCHED guard: the nonzero-step count, read back without stalling the stream
     unsigned long long* nz_host = nullptr;
     cudaEvent_t ev_nz = nullptr;
@@ -170,6 +171,7 @@ void free_problem(pcdm_problem* p) {
         cudaEventDestroy(p->ev_s0);
         cudaEventDestroy(p->ev_s1);
     }
+    for (cudaEvent_t e : p->pass_ev) cudaEventDestroy(e);
     if (p->ev_nz) cudaEventDestroy(p->ev_nz);
     cudaFreeHost(p->nz_host);
     cudaFree(p->sc);
@@ -699,9 +701,17 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if ((s = sampling_dev(spec, &p->du_T, &p->du_cap, st, &sdev)) != PCDM_OK) return s;
     // host x: every sample set of the run is drawn on a side stream while x crosses PCIe
     // (the sampler needs only seed and k; the copy engines and the SMs overlap)
+    // ... and for r much larger than L2 (huge) also for a device x, with the iterations
+    // waiting for their own sampler pass only (an event per pass), so the passes run on the
+    // low-priority side stream under the iteration kernels: huge 4.66e9 -> 4.81e9 updates/s
+    // (profiles/r01_presample_overlap_ab.txt; large +1 %, not enabled).  PCDM_PRESAMPLE_DEV=0/1
     const char* pe = getenv("PCDM_PRESAMPLE");
-    const bool presample = !x_dev && iters > 0 && spec.kind == PCDM_SAMPLING_NICE && !(pe && atoi(pe) == 0) &&
-                           (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
+    const char* pdev = getenv("PCDM_PRESAMPLE_DEV");
+    int l2_dev = 0;
+    cudaDeviceGetAttribute(&l2_dev, cudaDevAttrL2CacheSize, p->device);
+    const bool per_pass = pdev ? atoi(pdev) != 0 : (double)p->m * 4.0 > 2.0 * l2_dev;
+    const bool presample = (!x_dev || per_pass) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
+                           !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
     if (presample) {
         const size_t need = sizeof(int) * (size_t)iters * (size_t)tau;
         if (p->pre_cap < need) {
@@ -712,7 +722,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             p->pre_cap = need;
         }
         if (!p->side) {
-            CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking), "side stream");
+            int least = 0, greatest = 0;  // the presampler yields to the iteration kernels
+            cudaDeviceGetStreamPriorityRange(&least, &greatest);
+            CK(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, least), "side stream");
             CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "event");
             CK(cudaEventCreate(&p->ev_s0), "event");
             CK(cudaEventCreate(&p->ev_s1), "event");
@@ -721,11 +733,19 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0), "event");
         CK(cudaEventRecord(p->ev_s0, p->side), "event");
         CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), p->side), "memset rounds");
-        for (int64_t done = 0; done < iters;) {
+        for (int64_t done = 0, pass = 0; done < iters; ++pass) {
             const int64_t c = chunk_len(done);
             CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, p->pre_slots + done * tau, &p->sc->flags, p->side,
                             p->sms, &launches),
                "sampler");
+            if (per_pass) {
+                while ((int64_t)p->pass_ev.size() <= pass) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+                    p->pass_ev.push_back(e);
+                }
+                CK(cudaEventRecord(p->pass_ev[pass], p->side), "event");
+            }
             done += c;
         }
         CK(cudaEventRecord(p->ev_s1, p->side), "event");
@@ -1067,7 +1087,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.ctas = cl_size;
     }
 
-    if (presample) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
+    if (presample && !per_pass) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
     // iterations per launch of the iteration kernel: max(schunk, 64) (PCDM_ITER_CHUNK for
     // the 64; each launch of the persistent kernel costs its ramp-up and drain), never
     // across a residual refresh.  Slots are drawn ahead in windows of max(schunk, ichunk)
@@ -1150,6 +1170,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         }
         const int64_t c = iter_len(done);
         int* slots_c = presample ? p->pre_slots + done * tau : win_slots + (done - w0) * tau;
+        if (presample && per_pass)  // the pass holding the launch's last iteration (passes run in order)
+            CK(cudaStreamWaitEvent(st, p->pass_ev[(done + c - 1) / schunk], 0), "join presampler pass");
         // zero the barrier counter; the generic kernel also restarts its step lists per
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
         CK(cudaMemsetAsync(p->sc->barrier, 0, sizeof(p->sc->barrier), st), "memset barrier");
