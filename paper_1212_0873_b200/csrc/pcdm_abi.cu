@@ -701,15 +701,14 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if ((s = sampling_dev(spec, &p->du_T, &p->du_cap, st, &sdev)) != PCDM_OK) return s;
     // host x: every sample set of the run is drawn on a side stream while x crosses PCIe
     // (the sampler needs only seed and k; the copy engines and the SMs overlap)
-    // ... and for r much larger than L2 (huge) also for a device x, with the iterations
-    // waiting for their own sampler pass only (an event per pass), so the passes run on the
-    // low-priority side stream under the iteration kernels: huge 4.66e9 -> 4.81e9 updates/s
-    // (profiles/r01_presample_overlap_ab.txt; large +1 %, not enabled).  PCDM_PRESAMPLE_DEV=0/1
+    // ... and also for a device x, with the iterations waiting for their own sampler pass
+    // only (an event per pass), so the passes run on the low-priority side stream under
+    // the iteration kernels: huge 4.66e9 -> 4.81e9 updates/s, large / skewed 2^12 / tiny /
+    // kddb_like +1-1.5 %, medium and skewed 2^16 within -0.7 % (profiles/r01_presample_overlap_ab.txt).
+    // PCDM_PRESAMPLE_DEV=0: sample in the run's stream
     const char* pe = getenv("PCDM_PRESAMPLE");
     const char* pdev = getenv("PCDM_PRESAMPLE_DEV");
-    int l2_dev = 0;
-    cudaDeviceGetAttribute(&l2_dev, cudaDevAttrL2CacheSize, p->device);
-    const bool per_pass = pdev ? atoi(pdev) != 0 : (double)p->m * 4.0 > 2.0 * l2_dev;
+    const bool per_pass = pdev ? atoi(pdev) != 0 : true;
     const bool presample = (!x_dev || per_pass) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
                            !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
     if (presample) {
