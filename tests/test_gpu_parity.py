@@ -283,13 +283,18 @@ def test_packed_rejected_for_long_columns(gpu):
 
 
 # ------------------------------------------------------------------ many launches per run
+@pytest.mark.parametrize("presample", ["1", "0"], ids=["presampled", "in-stream"])
 @pytest.mark.parametrize("iter_chunk", ["3", "16"], ids=["launch-per-sampler-chunk", "launch-spans-chunks"])
-@pytest.mark.parametrize("variant", ["packed", "grid"])
-def test_many_chunks_per_run(gpu, monkeypatch, variant, iter_chunk):
+@pytest.mark.parametrize("variant", ["packed", "grid", "batched"])
+def test_many_chunks_per_run(gpu, monkeypatch, variant, iter_chunk, presample):
     # small sampler chunks force many sampler passes per run; iteration-kernel launches
-    # of 3 iterations, or of 16 whose slots come from several sampler chunks
+    # of 3 iterations, or of 16 whose slots come from several sampler chunks; the slots
+    # presampled on the side stream (each launch waiting on its own pass's event) or
+    # drawn in the run's stream window by window
     monkeypatch.setenv("PCDM_CHUNK", "3")
     monkeypatch.setenv("PCDM_ITER_CHUNK", iter_chunk)
+    monkeypatch.setenv("PCDM_BATCHED_CHUNK", iter_chunk)
+    monkeypatch.setenv("PCDM_PRESAMPLE_DEV", presample)
     c, r, v, b, lam = _ragged(3000, 2500, np.full(2500, 12), 12)
     for tau, iters, refresh in ((256, 61, 0), (2500, 7, 4), (33, 200, -1)):
         out = run_both(c, r, v, b, lam, 3000, tau, iters, seed=5, variant=variant, refresh_every=refresh)
