@@ -48,7 +48,11 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kBloomLog = 19;  // dirty-row filter: 2^19 bits = 64 KB of shared memory per CTA
 constexpr int kColLog = 16;    // stepped-column filter: 2^16 bits = 8 KB
-constexpr int kSweepMaxQ = 40;  // pass 2: slot ranges per CTA (x 2 KB of shared accumulators)
+#ifndef PCDM_EXPAND_THREADS
+#define PCDM_EXPAND_THREADS 512
+#endif
+constexpr int kExpandThreads = PCDM_EXPAND_THREADS;  // pass 1 CTA size (its slot range scales with it)
+constexpr int kSweepMaxSlots = 40 * 512;  // pass 2: slots per CTA (x 4 B of shared accumulators)
 #ifndef PCDM_SWEEP_HW
 #define PCDM_SWEEP_HW 16
 #endif
@@ -118,7 +122,7 @@ __device__ __forceinline__ bool bloom_test(const unsigned* bf, uint32_t v) {
 // ---------------------------------------------------------------- pass 1: expand + sort
 // Dynamic shared memory: stage int2[cq*maxe] | inv u16[cq*maxe] | cnt int[nb] | cur int[nb+1]
 template <int G>
-__global__ void __launch_bounds__(kThreads, PCDM_EXPAND_MINB) batch_expand_kernel(BatchedParams P) {
+__global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpandThreads) batch_expand_kernel(BatchedParams P) {
     constexpr int MAXE = 2 * (G - 1);
     extern __shared__ int4 s_raw[];
     const int cq = 1 << P.cq_log;
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, PCDM_EXPAND_MINB) batch_expand_kerne
         __syncthreads();
         // U slots per group in flight: the slot ids, then their blocks, then the entries
         constexpr int U = PCDM_EXPAND_U;
-        constexpr int GPC = kThreads / G;  // groups per CTA
+        constexpr int GPC = kExpandThreads / G;  // groups per CTA
         for (int sl0 = grp; sl0 < cq; sl0 += GPC * U) {
             int iv[U];
             int4 cv[U];
@@ -638,11 +642,11 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
     e = cudaFuncSetAttribute(batch_expand_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     if (e != cudaSuccess) return e;
     int per1 = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, batch_expand_kernel<G>, kThreads, sm1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, batch_expand_kernel<G>, kExpandThreads, sm1);
     const int g1 = std::min(P.nq, std::max(1, per1) * sms);
-    batch_expand_kernel<G><<<g1, kThreads, sm1, st>>>(P);
+    batch_expand_kernel<G><<<g1, kExpandThreads, sm1, st>>>(P);
     // pass 2: groups of qpc slot ranges per CTA, g0 accumulated in shared memory
-    const int qpc = std::max(1, std::min(kSweepMaxQ, (P.nq + 2 * sms - 1) / (2 * sms)));
+    const int qpc = std::max(1, std::min(kSweepMaxSlots >> P.cq_log, (P.nq + 2 * sms - 1) / (2 * sms)));
     const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float);
     const void* sw = P.logistic ? (const void*)batch_sweep_kernel<true> : (const void*)batch_sweep_kernel<false>;
     e = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
@@ -671,10 +675,11 @@ size_t batched_step_smem(int nhot) {
 }
 
 int batched_cq_log(int G) {
-    // Cq * maxlen_capacity <= 8192 entries staged in shared memory (64 KB + 16 KB)
+    // Cq * maxlen_capacity <= 8192 entries staged in shared memory (64 KB + 16 KB) for a
+    // 512-thread expand CTA, proportionally less for smaller ones
     const int maxe = 2 * (G - 1);
     int l = 0;
-    while (((2 << l) * maxe) <= 8192) ++l;
+    while (((2 << l) * maxe) <= 8192 * kExpandThreads / 512) ++l;
     return l;
 }
 
