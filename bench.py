@@ -43,16 +43,36 @@ VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", 6:
 KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
                      5: "batch_expand+batch_sweep+pcdm_batched_slot+batch_fold", 6: "pcdm_cluster_kernel",
                      -1: "pcdm_async_kernel"}
-# oracle iterations per reference step / cpu_baseline sample, per config
-REF_ITERS = {"tiny": 400, "medium": 200, "skewed": 20, "large": 8, "huge": 4, "logistic_small": 200, "kddb_like": 4}
+# The oracle timing sample, per config (one definition for the cpu_baseline of our
+# arm and for every step of --impl reference): iterations k = 0..K'-1 of the
+# config's run from x_0 = 0, on the columns they touch, O5-O8 loop time only.
 CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24, "logistic_small": 1000,
                       "kddb_like": 24}
+L2_PEAK = (18571.5, "measured: profiles/r01_microbench.jsonl stream_read over a 66 MB buffer (L2-resident), "
+                    "best of 100 reps")
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError):
+        ram = None
+    return {"host_cpu": model, "host_nproc": os.cpu_count(), "host_ram_gb": ram}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=list(I.CONFIGS) + list(I.LOGISTIC_CONFIGS),
@@ -69,6 +89,8 @@ def parse():
                     help="asynchronous variant (NEXT-4, PAPER.md:1248): tau*iters updates per step, no barriers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the oracle parity check of the first step (samples, omega, F, x)")
     a = ap.parse_args()
     if a.config is None:
         a.config = "kddb_like" if a.loss == "logistic" else "huge"
@@ -143,7 +165,7 @@ def job_throughput(units_per_rank_step, rank_ms_per_step, world):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -157,7 +179,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
             t0 = time.time()
@@ -202,16 +224,20 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config, variant, iters_per_launch):
-    """DRAM bytes per iteration-kernel launch from the committed ncu capture of this
-    config and loop ("<config>:<variant>"), if any."""
+def ncu_traffic(config, variant, sampling, iters_per_launch):
+    """DRAM (and L2) bytes per iteration-kernel launch from the committed ncu capture of
+    exactly this config, loop and sampling ("<config>:<loop>:<sampling>", written by
+    tools/ncu_traffic.py), or None when that combination was not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)["%s:%s" % (config, variant)]
-        return float(d["dram_bytes_per_iter"]) * iters_per_launch
+            d = json.load(f)["%s:%s:%s" % (config, variant, sampling)]
     except Exception:
         return None
+    out = {"dram": float(d["dram_bytes_per_iter"]) * iters_per_launch, "source": d.get("source")}
+    if d.get("l2_bytes_per_iter") is not None:
+        out["l2"] = float(d["l2_bytes_per_iter"]) * iters_per_launch
+    return out
 
 
 # ----------------------------------------------------------------------------- oracle sample
@@ -230,29 +256,23 @@ def oracle_sampling(args, tau):
     return None if args.sampling == "nice" else oracle.Sampling(args.sampling, tau, p_b=args.p_b)
 
 
-def oracle_subinstance(inst, tau, k0, k_iters, seed, osamp=None):
+def oracle_slots(tau, k0, k_iters, seed, n, osamp=None):
+    """The oracle's own slot arrays of S_k0..S_{k0+K-1} (int32[K, tau], -1 = idle)."""
+    import oracle
+    if osamp is None:
+        return oracle.samples(seed, k0, k_iters, tau, n)
+    return np.stack([oracle.sample_kind(osamp, seed, k, n) for k in range(k0, k0 + k_iters)])
+
+
+def oracle_subinstance(inst, tau, k0, k_iters, seed, osamp=None, slots=None):
     """Host CSC holding only the columns S_k0..S_{k0+K-1} touch (others empty),
     gathered from the resident instance; the slots come from the oracle's own
     sampler.  Test/baseline infrastructure: never on the product path."""
-    import oracle
-    n = inst.n
-    S = [oracle.sample(seed, k, tau, n) if osamp is None else oracle.sample_kind(osamp, seed, k, n)
-         for k in range(k0, k0 + k_iters)]
-    cols = np.unique(np.concatenate(S)).astype(np.int64)
-    cols = cols[cols >= 0]
-    dev = inst.colptr.device
-    ct = torch.from_numpy(cols).to(dev)
-    starts = inst.colptr[ct]
-    lens = inst.colptr[ct + 1] - starts
-    total = int(lens.sum())
-    offs = torch.cumsum(lens, 0) - lens
-    idx = torch.repeat_interleave(starts - offs, lens) + torch.arange(total, device=dev)
-    rows = inst.rowidx[idx].cpu().numpy()
-    vals = inst.val[idx].cpu().numpy()
-    full = np.zeros(n + 1, dtype=np.int64)
-    full[cols + 1] = lens.cpu().numpy()
-    np.cumsum(full, out=full)
-    return full, rows, vals, inst.b.cpu().numpy()
+    S = oracle_slots(tau, k0, k_iters, seed, inst.n, osamp) if slots is None else slots
+    cols = np.unique(S)
+    cols = cols[cols >= 0].astype(np.int64)
+    c, r, v = I.column_subset(inst.colptr, inst.rowidx, inst.val, cols)
+    return c, r, v, inst.b.cpu().numpy()
 
 
 def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None, osamp=None, loss="lasso"):
@@ -267,37 +287,115 @@ def run_oracle_sample(inst, tau, k0, k_iters, seed, sub=None, osamp=None, loss="
     return res.loop_seconds, sub
 
 
+def cpu_sample_note(kcpu, cfg, tau, secs):
+    return ("iterations k=0..%d of the %s run (tau=%d, seed 0, x_0 = 0) on the columns they touch; "
+            "O5-O8 loop time %.2f s" % (kcpu - 1, cfg.name, tau, secs))
+
+
+class ParityLeg:
+    """Oracle parity of the bench's own first step (iterations 0..iters-1 from x_0 = 0,
+    run seed 0): the oracle's slot arrays of every iteration, omega counted by the
+    oracle over the whole matrix, and the oracle run of the same iterations on the
+    columns they touch (alg:PCD1), forked into a background process
+    so that it overlaps the GPU measurement.  Nothing it compares against comes from
+    the CUDA path."""
+
+    def __init__(self, inst, tau, iters, osamp):
+        import tempfile
+
+        import oracle
+        from oracle.background import Job
+        self.iters, self.tau, self.n, self.osamp = iters, tau, inst.n, osamp
+        t0 = time.time()
+        self.S = oracle_slots(tau, 0, iters, 0, inst.n, osamp)
+        cols = np.unique(self.S)
+        self.cols = cols[cols >= 0].astype(np.int64)
+        colptr, rows, vals = I.column_subset(inst.colptr, inst.rowidx, inst.val, self.cols)
+        b = inst.b.cpu().numpy()
+        full_rows = inst.rowidx.cpu().numpy()
+        m, lam = inst.m, inst.lam
+        self.prep_s = time.time() - t0
+        self.tmp = tempfile.mkdtemp(prefix="pcdm_bench_parity_")
+        keep = self.cols
+
+        def fn():
+            om = oracle.omega(m, full_rows)  # O1 over the full matrix
+            res = oracle.run(m, colptr, rows, vals, b, lam, tau, iters, 0, omega_override=om, sampling=osamp)
+            F = oracle.objective(m, colptr, rows, vals, b, lam, res.x)
+            return dict(x=res.x[keep], F=np.float64(F), omega=np.int64(om), beta=np.float64(res.beta),
+                        loop_seconds=np.float64(res.loop_seconds))
+        self.job = Job("parity", fn, self.tmp)
+
+    def gpu_side(self, pcdm, prob, x, gsamp, dev):
+        """Right after the first step: the GPU's slot arrays, F and x."""
+        got = torch.empty(self.iters * self.tau, dtype=torch.int32, device=dev)
+        if gsamp is None:
+            pcdm.pcdm_sample(self.n, self.tau, 0, 0, self.iters, got)
+        else:
+            pcdm.pcdm_sample_sampling(self.n, gsamp, 0, 0, self.iters, got)
+        self.samples_bitexact = bool(np.array_equal(got.cpu().numpy().reshape(self.S.shape), self.S))
+        del got
+        self.S = None
+        self.F_gpu = prob.objective(x)
+        xh = x.cpu().numpy()
+        untouched = np.ones(xh.size, dtype=bool)
+        untouched[self.cols] = False
+        self.x_untouched_zero = not bool(np.any(xh[untouched]))
+        self.x_gpu = xh[self.cols].astype(np.float64)
+
+    def fields(self, omega_gpu):
+        import shutil
+        res = self.job.result()
+        shutil.rmtree(self.tmp, ignore_errors=True)
+        F_o = float(res["F"])
+        xo = res["x"]
+        scale = max(float(np.max(np.abs(xo))) if xo.size else 0.0, 1e-30)
+        dx = float(np.max(np.abs(self.x_gpu - xo))) / scale if xo.size else 0.0
+        relF = abs(self.F_gpu - F_o) / abs(F_o)
+        omega_ok = int(res["omega"]) == int(omega_gpu)
+        green = self.samples_bitexact and omega_ok and relF <= 1e-5 and dx <= 1e-4 and self.x_untouched_zero
+        return {"scope": "first step: iterations 0..%d from x_0 = 0, seed 0; oracle on the %d columns they touch, "
+                         "omega over the full matrix" % (self.iters - 1, self.cols.size),
+                "samples_bitexact": self.samples_bitexact, "omega_bitexact": omega_ok,
+                "omega_oracle": int(res["omega"]), "F_gpu": self.F_gpu, "F_oracle": F_o, "relF": relF,
+                "dx_rel": dx, "x_untouched_zero": self.x_untouched_zero,
+                "tolerance": {"relF": 1e-5, "dx_rel": 1e-4}, "status": "green" if green else "FAIL",
+                "oracle_loop_s": float(res["loop_seconds"]), "oracle_wall_s": float(res["wall_s"]),
+                "prep_s": self.prep_s}
+
+
 # ----------------------------------------------------------------------------- arms
 def bench_reference(args, world, rank):
     if rank != 0:
         return
     cfg = config_of(args)
     tau = args.tau or cfg.tau
-    kref = REF_ITERS[args.config]
-    dev = torch.device("cuda", 0)
+    kcpu = CPU_BASELINE_ITERS[args.config]
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
     inst = make_instance(args, dev)
     K, W = args.steps, args.warmup
     osamp = oracle_sampling(args, tau)
-    sub = oracle_subinstance(inst, tau, 0, kref * (K + W), seed=0, osamp=osamp)
+    sub = oracle_subinstance(inst, tau, 0, kcpu, seed=0, osamp=osamp)
     del inst.rowidx, inst.val
     secs = []
     for s in range(W + K):
-        t, _ = run_oracle_sample(inst, tau, s * kref, kref, 0, sub=sub, osamp=osamp, loss=args.loss)
+        t, _ = run_oracle_sample(inst, tau, 0, kcpu, 0, sub=sub, osamp=osamp, loss=args.loss)
         if s >= W:
             secs.append(t)
     step_s = sum(secs) / len(secs)
-    value = expected_size(args.sampling, tau, inst.n, args.p_b) * kref / step_s
+    value = expected_size(args.sampling, tau, inst.n, args.p_b) * kcpu / step_s
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": 1,
             "steps": K, "warmup": W, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "nnz_per_col": cfg.nnz_per_col,
-                       "tau": tau, "sampling": args.sampling, "iters_per_step": kref, "seed": 0,
-                       "note": "serial oracle on host cores; each step = %d iterations of the same run" % kref},
+                       "tau": tau, "sampling": args.sampling, "iters_per_step": kcpu, "seed": 0,
+                       "note": "serial oracle on one host core; every step is the same bounded sample as our "
+                               "arm's cpu_baseline"},
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "oracle",
-                             "sample": "iterations k=%d..%d of the %s run (columns they touch), O5-O8 loop only"
-                                       % (W * kref, (W + K) * kref - 1, cfg.name)},
+                             "sample": cpu_sample_note(kcpu, cfg, tau, step_s)},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "effective_GBps": value * cfg.nnz_per_col * BYTES_PER_NNZ / 1e9}
+    line.update(host_info())
     print(json.dumps(line), flush=True)
 
 
@@ -319,6 +417,14 @@ def bench_ours(args, world, rank, local):
     inst = make_instance(args, dev)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
+    gsamp = None if args.sampling == "nice" else pcdm.Sampling(args.sampling, tau, p_b=args.p_b)
+    osamp = oracle_sampling(args, tau) if rank == 0 and world == 1 else None
+    # oracle parity of the first step (run seed 0 = rank 0), started before create so the
+    # host copies are taken while device memory is free; it runs in the background
+    parity = None
+    do_parity = (rank == 0 and world == 1 and not args.no_parity and args.loss == "lasso" and not args.async_)
+    if do_parity:
+        parity = ParityLeg(inst, tau, iters, osamp)
     t0 = time.time()
     prob = pcdm.Problem(inst.m, inst.n, inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, loss=args.loss)
     create_s = time.time() - t0
@@ -331,14 +437,12 @@ def bench_ours(args, world, rank, local):
     sub = None
     do_cpu = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     kcpu = CPU_BASELINE_ITERS[args.config]
-    osamp = oracle_sampling(args, tau) if do_cpu else None
     if do_cpu:
         sub = oracle_subinstance(inst, tau, 0, kcpu, seed=0, osamp=osamp)
     del inst.rowidx, inst.val
     torch.cuda.empty_cache()
 
     run_seed = rank
-    gsamp = None if args.sampling == "nice" else pcdm.Sampling(args.sampling, tau, p_b=args.p_b)
     size = expected_size(args.sampling, tau, inst.n, args.p_b)
     x = torch.zeros(inst.n, dtype=torch.float32, device=dev)
     flush = torch.empty(int(2 * l2_bytes) // 4, dtype=torch.float32, device=dev) \
@@ -355,8 +459,11 @@ def bench_ours(args, world, rank, local):
                  stream=stream)
         step += 1
 
-    for _ in range(W):
+    for w in range(W):
         one_step(x)
+        if w == 0 and parity is not None:
+            torch.cuda.synchronize()
+            parity.gpu_side(pcdm, prob, x, gsamp, dev)
     torch.cuda.synchronize()
     barrier(world)
     clocks = ClockSampler(local)
@@ -388,9 +495,18 @@ def bench_ours(args, world, rank, local):
     alg_bytes_launch = BYTES_PER_NNZ * avg_c * size * iters_per_launch
     launch_ms = it_ms / max(it_launches, 1)
     achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
-    peak, peak_src = hbm_peak()
+    # bound: HBM when r (gathered and scattered every iteration) does not fit in L2,
+    # else the L2 (A streams from HBM or sits in L2, r is served by L2)
+    r_in_l2 = 4 * inst.m <= l2_bytes // 2
+    hpeak, hpeak_src = hbm_peak()
+    peak, peak_src = (L2_PEAK if r_in_l2 else (hpeak, hpeak_src))
+    samp_key = args.sampling if args.sampling != "binomial" else "binomial%g" % args.p_b
     traffic = None if args.async_ else ncu_traffic(cfg.name, VARIANT_NAMES.get(st_list[-1]["variant"], "?"),
-                                                    iters_per_launch)
+                                                    samp_key, iters_per_launch)
+    # ncu traffic of the bounding memory level: DRAM bytes for HBM-bound runs, L2 bytes
+    # (lts__t_bytes) for L2-bound ones
+    traffic_kind = ("l2" if r_in_l2 else "dram") if traffic else None
+    traffic_bytes = traffic.get(traffic_kind) if traffic else None
     launches = sum(s["kernel_launches"] for s in st_list)
     nz = sum(s["nonzero_deltas"] for s in st_list)
 
@@ -420,10 +536,12 @@ def bench_ours(args, world, rank, local):
 
     cpu = None
     if do_cpu:
+        if parity is not None:
+            parity.job.result()  # the timing sample runs alone on the host
         secs, _ = run_oracle_sample(inst, tau, 0, kcpu, 0, sub=sub, osamp=osamp, loss=args.loss)
         cpu = {"value": size * kcpu / secs, "unit": "updates/s", "cores": 1, "kind": "oracle",
-               "sample": "iterations k=0..%d of the %s run (tau=%d) on the columns they touch; "
-                         "O5-O8 loop time %.2f s" % (kcpu - 1, cfg.name, tau, secs)}
+               "sample": cpu_sample_note(kcpu, cfg, tau, secs)}
+    par = parity.fields(prob.omega) if parity is not None else None
 
     if rank != 0:
         return
@@ -439,10 +557,14 @@ def bench_ours(args, world, rank, local):
                    "l2": ("inputs larger than L2 (A %.1f GB vs L2 %.0f MB)" % (nnz * 8 / 1e9, l2_bytes / 1e6))
                    if flush is None else "L2 flushed between timed steps"},
         "effective_GBps": value * avg_c * BYTES_PER_NNZ / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "traffic_GBps": traffic / (launch_ms / 1e3) / 1e9 if traffic else None,
-                     "traffic_frac": traffic / (launch_ms / 1e3) / 1e9 / peak if traffic else None,
+        "roofline": {"bound": "l2" if r_in_l2 else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic_bytes, "peak_source": peak_src,
+                     "traffic_kind": traffic_kind, "traffic_source": traffic["source"] if traffic else None,
+                     "traffic_GBps": traffic_bytes / (launch_ms / 1e3) / 1e9 if traffic_bytes else None,
+                     "traffic_frac": traffic_bytes / (launch_ms / 1e3) / 1e9 / peak if traffic_bytes else None,
+                     "dram_traffic_frac_of_hbm": traffic["dram"] / (launch_ms / 1e3) / 1e9 / hpeak
+                     if traffic else None,
+                     "hbm_peak": hpeak,
                      "kernel": KERNEL_OF_VARIANT.get(st0["variant"], "?"), "algorithmic_bytes_per_launch": alg_bytes_launch,
                      "launch_ms": launch_ms, "iters_per_launch": iters_per_launch,
                      "share_of_step": it_ms / max(sum(step_ms), 1e-9)},
@@ -457,8 +579,10 @@ def bench_ours(args, world, rank, local):
         "variant": VARIANT_NAMES.get(st0["variant"], "?"),
         "grid": {"ctas": st0["grid_ctas"], "threads": st0["threads_per_cta"], "lanes_per_column": st0["lanes_per_column"]},
         "setup_s": {"generate": gen_s, "create": create_s},
+        "parity": par,
         "context": "paper: 2e10-nnz LASSO in ~2 h on 24 cores (~4.8e6 updates/s, asynchronous, PAPER.md:1237,1248)",
     }
+    line.update(host_info())
     print(json.dumps(line), flush=True)
     prob.close()
 

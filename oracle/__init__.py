@@ -119,12 +119,26 @@ def draw(seed: int, k: int, rho: int, j: int, tag: int, n: int):
     return int(v.value) if ok else None
 
 
-def sample(seed: int, k: int, tau: int, n: int) -> np.ndarray:
-    """O5: slot array of S_k (tau distinct indices in [0, n))."""
+def sample(seed: int, k: int, tau: int, n: int, workspace: np.ndarray = None) -> np.ndarray:
+    """O5: slot array of S_k (tau distinct indices in [0, n)).
+    workspace: optional zeroed uint8[n] scratch (or_sample's `taken`, left zeroed),
+    so that many calls on a large n do not each allocate n bytes."""
     out = np.empty(tau, dtype=np.int32)
-    rc = _load().or_sample(seed, k, tau, n, _ptr(out), None)
+    if workspace is not None and (workspace.dtype != np.uint8 or workspace.size < n
+                                  or not workspace.flags.c_contiguous):
+        raise ValueError("workspace must be a contiguous zeroed uint8[n]")
+    rc = _load().or_sample(seed, k, tau, n, _ptr(out), None if workspace is None else _ptr(workspace))
     if rc != 0:
         raise ValueError("or_sample failed (rc=%d)" % rc)
+    return out
+
+
+def samples(seed: int, k0: int, count: int, tau: int, n: int) -> np.ndarray:
+    """O5 for k = k0 .. k0+count-1: int32[count, tau], row k-k0 = slot array of S_k."""
+    ws = np.zeros(n, dtype=np.uint8)
+    out = np.empty((count, tau), dtype=np.int32)
+    for t in range(count):
+        out[t] = sample(seed, k0 + t, tau, n, workspace=ws)
     return out
 
 

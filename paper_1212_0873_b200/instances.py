@@ -166,6 +166,46 @@ def generate(cfg: InstanceConfig | str, seed: int = 0, device="cpu",
     return Instance(cfg, m, n, colptr, rowidx, val, b, lam, xs_idx, xs_val.to(torch.float32))
 
 
+def column_subset(colptr: torch.Tensor, rowidx: torch.Tensor, val: torch.Tensor, cols,
+                  chunk_entries: int = 1 << 26):
+    """Host CSC of the same m x n shape that keeps only the columns ``cols``
+    (sorted unique int64 indices) of (colptr, rowidx, val) and leaves every other
+    column empty: (colptr int64[n+1], rowidx int32, val f32) as numpy arrays.
+    Pure data movement (no method arithmetic); gathers on the arrays' device in
+    chunks of about ``chunk_entries`` entries so a multi-GB subset needs little
+    scratch.  Used to hand the oracle the part of a large instance a run touches."""
+    import numpy as np
+    dev = colptr.device
+    n = colptr.numel() - 1
+    cols_np = np.asarray(cols, dtype=np.int64)
+    ct_all = torch.from_numpy(cols_np).to(dev)
+    lens_all = colptr[ct_all + 1] - colptr[ct_all]
+    full = np.zeros(n + 1, dtype=np.int64)
+    full[cols_np + 1] = lens_all.cpu().numpy()
+    np.cumsum(full, out=full)
+    total = int(full[-1])
+    rows = np.empty(total, dtype=np.int32)
+    vals = np.empty(total, dtype=np.float32)
+    csum = torch.cumsum(lens_all, 0)
+    c0, out0 = 0, 0
+    while c0 < cols_np.size:
+        base = int(csum[c0 - 1]) if c0 else 0
+        c1 = int(torch.searchsorted(csum, base + chunk_entries, right=True))
+        c1 = max(c1, c0 + 1)
+        ct, lens = ct_all[c0:c1], lens_all[c0:c1]
+        starts = colptr[ct]
+        cnt = int(lens.sum())
+        offs = torch.cumsum(lens, 0) - lens
+        idx = torch.repeat_interleave(starts - offs, lens) + torch.arange(cnt, device=dev)
+        rows[out0:out0 + cnt] = rowidx[idx].cpu().numpy()
+        vals[out0:out0 + cnt] = val[idx].cpu().numpy()
+        out0 += cnt
+        c0 = c1
+        del idx, starts, offs
+    assert out0 == total
+    return full, rows, vals
+
+
 def random_csc(m: int, n: int, col_lengths, seed: int = 0, device="cpu",
                values: str = "normal"):
     """Small ragged CSC for edge-case tests: column i gets col_lengths[i]
