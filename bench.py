@@ -47,7 +47,7 @@ KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter
 # arm and for every step of --impl reference): iterations k = 0..K'-1 of the
 # config's run from x_0 = 0, on the columns they touch, O5-O8 loop time only.
 CPU_BASELINE_ITERS = {"tiny": 2000, "medium": 2000, "skewed": 200, "large": 60, "huge": 24, "logistic_small": 1000,
-                      "kddb_like": 24}
+                      "kddb_like": 24, "ragged": 60, "ragged_small": 400}
 L2_PEAK = (18571.5, "measured: profiles/r01_microbench.jsonl stream_read over a 66 MB buffer (L2-resident), "
                     "best of 100 reps")
 
@@ -75,7 +75,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=list(I.CONFIGS) + list(I.LOGISTIC_CONFIGS),
+    ap.add_argument("--config", default=None,
+                    choices=list(I.CONFIGS) + list(I.RAGGED_CONFIGS) + list(I.LOGISTIC_CONFIGS),
                     help="default: huge (LASSO) / kddb_like (logistic)")
     ap.add_argument("--loss", default="lasso", choices=["lasso", "logistic"],
                     help="logistic: the L2-regularised logistic problem of Sec. 8.4 (NEXT-3)")
@@ -113,11 +114,13 @@ class LogisticInstance:
 def make_instance(args, device):
     if args.loss == "logistic":
         return LogisticInstance(args.config, device)
-    return I.generate(I.CONFIGS[args.config], seed=0, device=device)
+    return I.generate(config_of(args), seed=0, device=device)
 
 
 def config_of(args):
-    return I.LOGISTIC_CONFIGS[args.config] if args.loss == "logistic" else I.CONFIGS[args.config]
+    if args.loss == "logistic":
+        return I.LOGISTIC_CONFIGS[args.config]
+    return I.CONFIGS[args.config] if args.config in I.CONFIGS else I.RAGGED_CONFIGS[args.config]
 
 
 # ----------------------------------------------------------------------------- dist
@@ -373,6 +376,7 @@ def bench_reference(args, world, rank):
     kcpu = CPU_BASELINE_ITERS[args.config]
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
     inst = make_instance(args, dev)
+    avg_c = inst.nnz / inst.n
     K, W = args.steps, args.warmup
     osamp = oracle_sampling(args, tau)
     sub = oracle_subinstance(inst, tau, 0, kcpu, seed=0, osamp=osamp)
@@ -394,7 +398,7 @@ def bench_reference(args, world, rank):
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "oracle",
                              "sample": cpu_sample_note(kcpu, cfg, tau, step_s)},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "effective_GBps": value * cfg.nnz_per_col * BYTES_PER_NNZ / 1e9}
+            "effective_GBps": value * avg_c * BYTES_PER_NNZ / 1e9}
     line.update(host_info())
     print(json.dumps(line), flush=True)
 
@@ -550,7 +554,9 @@ def bench_ours(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "nnz": nnz, "nnz_per_col": cfg.nnz_per_col,
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "nnz": nnz, "nnz_per_col": cfg.nnz_per_col
+                   if cfg.col_lengths == "fixed" else "pareto(alpha=%g, %d..%d), mean %.2f"
+                   % (cfg.len_alpha, cfg.len_min, cfg.len_max, avg_c),
                    "rows": cfg.rows, "tau": tau, "iters_per_step": iters, "seed_instance": 0, "loss": args.loss,
                    "sampling": args.sampling if args.sampling != "binomial" else "binomial(p_b=%g)" % args.p_b,
                    "seed_run": "rank", "parallelism": "replicas" if world > 1 else "single",

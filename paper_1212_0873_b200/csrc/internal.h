@@ -27,6 +27,7 @@ cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms
 struct XHeaders {
     int4* blocks;
     int G;
+    const long long* off;  // ragged layout: chunk offset of column i (nullptr: uniform, i * G)
     int* list;
     unsigned long long* count;
     int64_t cap;
@@ -153,12 +154,30 @@ struct PackedParams {
                           //      global atomic per CTA and iteration (dense-step workloads)
     int hot_cache;        // 1: copy r_k[hot_rows] into shared memory every iteration (else
                           //    hot entries are gathered through the row table)
+    // ragged layout (kernels_ragged.cu): per iteration the slots binned by class
+    const int2* bins;     // [iters][tau] {i, chunk offset of column i}, grouped by class
+    const int* bcnt;      // [iters][8] class starts (2, 4, 8, 16, 32 lanes, warp-long, CTA-long) and end
 };
-cudaError_t launch_xhdr_clear(int4* blocks, int G, const int* list, const unsigned long long* count, int64_t cap,
-                              int64_t n, cudaStream_t st, int sms, int64_t* launches);
-cudaError_t launch_xhdr_out(const int4* blocks, int G, float* x, int64_t n, const int* list,
+cudaError_t launch_xhdr_clear(int4* blocks, int G, const long long* off, const int* list,
+                              const unsigned long long* count, int64_t cap, int64_t n, cudaStream_t st, int sms,
+                              int64_t* launches);
+cudaError_t launch_xhdr_out(const int4* blocks, int G, const long long* off, float* x, int64_t n, const int* list,
                             const unsigned long long* count, int64_t cap, cudaStream_t st, int sms,
                             int64_t* launches);
+// ---- ragged layout (kernels_ragged.cu): a warp, sub-warp or CTA per sampled column by its length
+// off[n+1] chunk offsets (g_i = pow2 >= 1 + ceil(len/2) for len <= 62, 1 + ceil(len/2) beyond);
+// fails with cudaErrorInvalidValue when the blocks would exceed 2^32 chunks
+// cls[n]: class of each column (0..4: 2..32 lanes, 5: warp-long, 6: CTA-long)
+cudaError_t build_ragged(const DevCSC& A, const float* L, const int* hot_rows, int nhot, long long** off_out,
+                         unsigned char** cls_out, int4** blocks_out, long long* total_out, cudaStream_t st, int sms,
+                         int64_t* launches);
+size_t bin_scratch_bytes(int64_t count);
+// slots [count][tau] -> bins [count][tau] {i, off[i]} grouped by class, bcnt [count][8]
+cudaError_t bin_chunk(const int* slots, int64_t tau, int64_t count, const long long* off, const unsigned char* cls,
+                      int* scratch, int2* bins, int* bcnt, cudaStream_t st, int sms, int64_t* launches);
+size_t ragged_smem_bytes(int nhot);
+int ragged_ctas(int sms, bool logistic, int nhot);
+cudaError_t launch_ragged(int ctas, const PackedParams& P, cudaStream_t st, int64_t* launches);
 // asynchronous variant (NEXT-4): no barriers, no sampler pass
 struct AsyncParams {
     const int4* blocks;

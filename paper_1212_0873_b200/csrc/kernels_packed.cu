@@ -357,18 +357,20 @@ __global__ void __launch_bounds__(kThreads, 3) pcdm_async_kernel(AsyncParams A) 
 // during the run every changed i is appended;
 // refresh / run end: x_i = header for i in D.  If D overflows its capacity the
 // start / end passes walk all n columns instead.
-__global__ void xhdr_clear_kernel(int4* __restrict__ blocks, int G, const int* __restrict__ list,
+__global__ void xhdr_clear_kernel(int4* __restrict__ blocks, int G, const long long* __restrict__ off,
+                                  const int* __restrict__ list,
                                   const unsigned long long* __restrict__ count, int64_t cap, int64_t n) {
     const unsigned long long c = *count;
     const bool all = c > (unsigned long long)cap;
     const int64_t total = all ? n : (int64_t)c;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = all ? t : list[t];
-        ((float*)(blocks + i * G))[2] = 0.0f;
+        ((float*)(blocks + (off ? off[i] : i * G)))[2] = 0.0f;
     }
 }
 
-__global__ void xhdr_out_kernel(const int4* __restrict__ blocks, int G, float* __restrict__ x, int64_t n,
+__global__ void xhdr_out_kernel(const int4* __restrict__ blocks, int G, const long long* __restrict__ off,
+                                float* __restrict__ x, int64_t n,
                                 const int* __restrict__ list, const unsigned long long* __restrict__ count,
                                 int64_t cap) {
     const unsigned long long c = *count;
@@ -376,7 +378,7 @@ __global__ void xhdr_out_kernel(const int4* __restrict__ blocks, int G, float* _
     const int64_t total = all ? n : (int64_t)c;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = all ? t : list[t];
-        x[i] = __ldcg((const float*)(blocks + i * G) + 2);
+        x[i] = __ldcg((const float*)(blocks + (off ? off[i] : i * G)) + 2);
     }
 }
 
@@ -488,17 +490,18 @@ cudaError_t launch_sel(int G, int ctas, const PackedParams& P, cudaStream_t st) 
 
 namespace pcdm_internal {
 
-cudaError_t launch_xhdr_clear(int4* blocks, int G, const int* list, const unsigned long long* count, int64_t cap,
-                              int64_t n, cudaStream_t st, int sms, int64_t* launches) {
-    xhdr_clear_kernel<<<sms * 8, 256, 0, st>>>(blocks, G, list, count, cap, n);
+cudaError_t launch_xhdr_clear(int4* blocks, int G, const long long* off, const int* list,
+                              const unsigned long long* count, int64_t cap, int64_t n, cudaStream_t st, int sms,
+                              int64_t* launches) {
+    xhdr_clear_kernel<<<sms * 8, 256, 0, st>>>(blocks, G, off, list, count, cap, n);
     ++*launches;
     return cudaGetLastError();
 }
 
-cudaError_t launch_xhdr_out(const int4* blocks, int G, float* x, int64_t n, const int* list,
+cudaError_t launch_xhdr_out(const int4* blocks, int G, const long long* off, float* x, int64_t n, const int* list,
                             const unsigned long long* count, int64_t cap, cudaStream_t st, int sms,
                             int64_t* launches) {
-    xhdr_out_kernel<<<sms * 8, 256, 0, st>>>(blocks, G, x, n, list, count, cap);
+    xhdr_out_kernel<<<sms * 8, 256, 0, st>>>(blocks, G, off, x, n, list, count, cap);
     ++*launches;
     return cudaGetLastError();
 }

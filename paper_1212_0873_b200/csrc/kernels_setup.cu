@@ -138,7 +138,7 @@ __device__ __forceinline__ void scatter_col(int64_t i, float xi, const long long
         return;
     }
     if (xh.blocks) {
-        ((float*)(xh.blocks + i * xh.G))[2] = xi;
+        ((float*)(xh.blocks + (xh.off ? xh.off[i] : i * xh.G)))[2] = xi;
         if (xh.cap > 0) {  // 0: dense iterate, no dirty list
             const unsigned long long q = atomicAdd(xh.count, 1ull);
             if (q < (unsigned long long)xh.cap) xh.list[q] = (int)i;
@@ -386,7 +386,7 @@ cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms
 
 cudaError_t launch_residual64(const DevCSC& A, const float* b, const float* x, double* r64, int* flags,
                               cudaStream_t st, int sms, int64_t* launches, const XHeaders* xh, const DevCSR* csr) {
-    const XHeaders none{nullptr, 0, nullptr, nullptr, 0};
+    const XHeaders none{nullptr, 0, nullptr, nullptr, nullptr, 0};
     if (csr) {
         scatter_x_kernel<<<grid_for((A.n + 3) / 4, kThreads, sms * 8), kThreads, 0, st>>>(
             A.n, (const long long*)A.colptr, A.rowidx, A.val, x, r64, flags, xh ? *xh : none, false);

@@ -87,7 +87,19 @@ struct pcdm_problem {
     int* xlist = nullptr;      // dirty list D of columns whose block header may hold x_i != 0
     unsigned long long* xlist_count = nullptr;  // |D| (> cap: overflowed, walk all n)
     int64_t xlist_cap = 0;
-    int packed_G = 0;          // 0: no packed copy (a column longer than 62 entries)
+    int packed_G = 0;          // uniform packed layout: lanes per column (0: none)
+    // RAGGED packed layout (kernels_ragged.cu): column i at chunk offset blk_off[i], a warp,
+    // sub-warp or CTA per sampled column by its length; chosen at create when a column is
+    // longer than 62 entries or the longest column would at least double every column's lanes
+    bool ragged = false;
+    long long* blk_off = nullptr;
+    unsigned char* blk_cls = nullptr;
+    long long ragged_chunks = 0;
+    int* bin_scr = nullptr;    // binning scratch of one sampler pass
+    size_t bin_scr_cap = 0;
+    int2* bins = nullptr;      // binned slot entries of the run's sampled windows / presampled run
+    int* bcnt = nullptr;
+    size_t bins_cap = 0;       // entries
     int* hot_rows = nullptr;   // ascending ids of the hot rows cached in shared memory (packed loop)
     int nhot = 0;
     int64_t hot_max_count = 0; // stored entries of the most frequent row
@@ -148,6 +160,11 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->r64);
     cudaFree(p->r2);
     cudaFree(p->blocks);
+    cudaFree(p->blk_off);
+    cudaFree(p->blk_cls);
+    cudaFree(p->bin_scr);
+    cudaFree(p->bins);
+    cudaFree(p->bcnt);
     cudaFree(p->hot_rows);
     if (p->has_csr) {
         cudaFree((void*)p->csr.rowptr);
@@ -582,7 +599,24 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         if ((e = launch_max_len(n, p->colptr, &p->sc->max_out, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "max len"); break; }
         if ((s = read_scalars(p, &hs, st)) != PCDM_OK) break;
         p->max_len = hs.max_out;
-        if (p->max_len <= 62 && !getenv("PCDM_NO_PACK")) {
+        // layout: uniform G x 16 B blocks when every column fits 62 entries and the longest
+        // column does not at least double the lanes of an average one; ragged otherwise
+        // (PCDM_LAYOUT=uniform|ragged forces one, for tests and A/B runs)
+        const int64_t avg_len = (nnz + n - 1) / n;
+        const char* lay = getenv("PCDM_LAYOUT");
+        bool want_ragged = lay ? strcmp(lay, "ragged") == 0
+                               : (p->max_len > 62 || packed_lanes(p->max_len) > 2 * packed_lanes(avg_len));
+        if (want_ragged && !getenv("PCDM_NO_PACK")) {
+            e = build_ragged(p->csc(), p->L, p->hot_rows, p->nhot, &p->blk_off, &p->blk_cls, &p->blocks,
+                             &p->ragged_chunks, st, p->sms, &launches);
+            if (e == cudaSuccess) {
+                p->ragged = true;
+            } else {
+                cudaGetLastError();  // too large / out of memory: the uniform layout or none
+                want_ragged = false;
+            }
+        }
+        if (!p->ragged && p->max_len <= 62 && !getenv("PCDM_NO_PACK")) {
             const int G = packed_lanes(p->max_len);
             if (cudaMalloc((void**)&p->blocks, (size_t)n * G * 16) == cudaSuccess) {
                 p->packed_G = G;
@@ -666,9 +700,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
     if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
     if (variant < 0 || variant > 6) return fail(PCDM_EINVAL, "unknown variant %d", variant);
-    if ((variant == PCDM_VARIANT_PACKED || variant == PCDM_VARIANT_BATCHED || variant == PCDM_VARIANT_CLUSTER) &&
-        !p->packed_G)
-        return fail(PCDM_EINVAL, "PACKED variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
+    if (variant == PCDM_VARIANT_PACKED && !p->packed_G && !p->ragged)
+        return fail(PCDM_EINVAL, "PACKED variant: no packed copy of A (device memory)");
+    if ((variant == PCDM_VARIANT_BATCHED || variant == PCDM_VARIANT_CLUSTER) && !p->packed_G)
+        return fail(PCDM_EINVAL, "BATCHED / CLUSTER variants need the uniform packed layout (max column length %lld%s)",
+                    (long long)p->max_len, p->ragged ? ", ragged layout" : "");
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
@@ -711,6 +747,32 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const bool per_pass = pdev ? atoi(pdev) != 0 : true;
     const bool presample = (!x_dev || per_pass) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
                            !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
+    // ragged layout: the slot arrays are binned by column class; with presampling the
+    // binning rides on each sampler pass (side stream), else it runs before each launch
+    const IterLaunch plan0 = plan_iter(variant >= PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n,
+                                       p->nnz, tau, p->sms, p->device, p->loss == 1);
+    const bool ragged_plan = p->ragged && (variant == PCDM_VARIANT_PACKED ||
+                                           (variant == PCDM_VARIANT_AUTO && plan0.variant == PCDM_VARIANT_GRID));
+    auto ensure_bins = [&](int64_t its, int64_t scr_its) -> pcdm_status {
+        if (p->bins_cap < (size_t)(its * tau)) {
+            cudaFree(p->bins);
+            cudaFree(p->bcnt);
+            p->bins = nullptr;
+            p->bcnt = nullptr;
+            p->bins_cap = 0;
+            CK(cudaMalloc((void**)&p->bins, sizeof(int2) * its * tau), "alloc bins");
+            CK(cudaMalloc((void**)&p->bcnt, sizeof(int) * 8 * its), "alloc bins");
+            p->bins_cap = (size_t)(its * tau);
+        }
+        if (p->bin_scr_cap < bin_scratch_bytes(scr_its)) {
+            cudaFree(p->bin_scr);
+            p->bin_scr = nullptr;
+            p->bin_scr_cap = 0;
+            CK(cudaMalloc((void**)&p->bin_scr, bin_scratch_bytes(scr_its)), "alloc bin scratch");
+            p->bin_scr_cap = bin_scratch_bytes(scr_its);
+        }
+        return PCDM_OK;
+    };
     if (presample) {
         const size_t need = sizeof(int) * (size_t)iters * (size_t)tau;
         if (p->pre_cap < need) {
@@ -732,11 +794,16 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0), "event");
         CK(cudaEventRecord(p->ev_s0, p->side), "event");
         CK(cudaMemsetAsync(sp.w.rounds_max, 0, sizeof(int), p->side), "memset rounds");
+        if (ragged_plan && (s = ensure_bins(iters, schunk)) != PCDM_OK) return s;
         for (int64_t done = 0, pass = 0; done < iters; ++pass) {
             const int64_t c = chunk_len(done);
             CK(sample_chunk(sp.w, sdev, seed, first_iter + done, c, p->pre_slots + done * tau, &p->sc->flags, p->side,
                             p->sms, &launches),
                "sampler");
+            if (ragged_plan)
+                CK(bin_chunk(p->pre_slots + done * tau, tau, c, p->blk_off, p->blk_cls, p->bin_scr, p->bins + done * tau,
+                             p->bcnt + done * 8, p->side, p->sms, &launches),
+                   "binning");
             if (per_pass) {
                 while ((int64_t)p->pass_ev.size() <= pass) {
                     cudaEvent_t e;
@@ -760,10 +827,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
 
     double beta_d = sampling_beta(spec, p->omega, p->n);
     if (beta_override > 0.0) beta_d = beta_override;
-    IterLaunch plan = plan_iter(variant >= PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n, p->nnz, tau,
-                                p->sms, p->device, p->loss == 1);
+    IterLaunch plan = plan0;
     // AUTO: packed blocks whenever the shared-memory variant does not apply
-    bool packed = p->packed_G > 0 &&
+    bool packed = (p->packed_G > 0 || p->ragged) &&
                   (variant >= PCDM_VARIANT_PACKED || (variant == PCDM_VARIANT_AUTO && plan.variant == PCDM_VARIANT_GRID));
     // BATCHED (kernels_batched.cu): AUTO picks it for LASSO when r is much larger than L2
     // (huge: 3.90e9 -> 4.60e9 updates/s; large, skewed, kddb_like stay on the packed loop,
@@ -786,15 +852,15 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const bool auto_batched =
         variant == PCDM_VARIANT_AUTO &&
         (bat_env ? atoi(bat_env) != 0
-                 : p->loss == 0 && p->packed_G <= 8 && (double)p->m * 4.0 > 2.0 * l2_bytes && es1 >= min_slots &&
+                 : p->loss == 0 && p->packed_G > 0 && p->packed_G <= 8 && (double)p->m * 4.0 > 2.0 * l2_bytes && es1 >= min_slots &&
                        es1 >= 0.8 * (double)tau);
-    bool batched = packed && (variant == PCDM_VARIANT_BATCHED || auto_batched);
+    bool batched = packed && p->packed_G > 0 && (variant == PCDM_VARIANT_BATCHED || auto_batched);
     const bool bat_fallback = batched && variant == PCDM_VARIANT_AUTO;
     if (batched && !bat_fallback) packed = false;
     // CLUSTER (kernels_cluster.cu): r in one cluster's distributed shared memory
     int cl_size = 0, cl_rpc = 0, cl_cap = 0;
     size_t cl_smem = 0;
-    if (packed && !batched && (variant == PCDM_VARIANT_CLUSTER || variant == PCDM_VARIANT_AUTO)) {
+    if (packed && !batched && p->packed_G > 0 && (variant == PCDM_VARIANT_CLUSTER || variant == PCDM_VARIANT_AUTO)) {
         // AUTO only with PCDM_CLUSTER=1: measured slower than the grid loop on medium
         // (5.0 vs 3.8 us per iteration, profiles/r01_cluster_medium_ab.jsonl)
         const char* ce = getenv("PCDM_CLUSTER");
@@ -824,7 +890,32 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     bool one_barrier = false;
     int list_cap = 0;
     int cluster_sync = 0;
-    if (packed) {
+    const bool ragged_run = packed && p->ragged;
+    if (ragged_run) {
+        // one barrier per iteration with the double-buffered residual (the generic CSC
+        // kernel if the second buffer cannot be allocated)
+        one_barrier = true;
+        if (!p->r2 && cudaMalloc((void**)&p->r2, sizeof(float) * p->m) != cudaSuccess) {
+            cudaGetLastError();
+            p->r2 = nullptr;
+            one_barrier = false;
+            packed = false;
+        }
+    }
+    if (packed && ragged_run) {
+        plan.variant = PCDM_VARIANT_PACKED;
+        plan.lanes = 0;  // per column: 2..32 lanes, or a CTA beyond 62 entries
+        plan.threads = 512;
+        plan.ctas = ragged_ctas(p->sms, p->loss == 1, p->nhot);
+        // small tau: only about as many CTAs as the average column needs lanes
+        const double gavg = (double)p->ragged_chunks / (double)p->n;
+        const int64_t busy = std::max<int64_t>(1, (int64_t)ceil((double)tau * gavg / plan.threads));
+        if (busy < plan.ctas) plan.ctas = (int)busy;
+        if (const char* cs = getenv("PCDM_CTAS")) {
+            const int v = atoi(cs);
+            if (v >= 1) plan.ctas = std::min(v, ragged_ctas(p->sms, p->loss == 1, p->nhot));
+        }
+    } else if (packed) {
         // one barrier per iteration (double-buffered r, the previous iteration's steps
         // replayed): measured faster on every config (huge: 45.7 -> 44.2 ms/step,
         // profiles/r01_one_barrier_huge_ab.log); two barriers if the second buffer
@@ -908,12 +999,12 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
             p->xlist_cap = cap;
         }
-        CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, p->xlist_cap, p->n, st, p->sms,
+        CK(launch_xhdr_clear(p->blocks, p->packed_G, p->blk_off, p->xlist, p->xlist_count, p->xlist_cap, p->n, st, p->sms,
                              &launches),
            "x headers");
         cap_eff = xdense ? 0 : p->xlist_cap;
         CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
-        xh = XHeaders{p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff};
+        xh = XHeaders{p->blocks, p->packed_G, p->blk_off, p->xlist, p->xlist_count, cap_eff};
     }
     if ((s = residual_from(p, xd, st, &launches, xhdr ? &xh : nullptr, one_barrier && !batched ? p->r2 : nullptr)) !=
         PCDM_OK)
@@ -923,7 +1014,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (hs.flags & FLAG_NONFINITE_X) return fail(PCDM_EINVAL, "non-finite value in x");
     auto x_out = [&]() -> pcdm_status {
         if (xhdr)
-            CK(launch_xhdr_out(p->blocks, p->packed_G, xd, p->n, p->xlist, p->xlist_count, cap_eff, st, p->sms,
+            CK(launch_xhdr_out(p->blocks, p->packed_G, p->blk_off, xd, p->n, p->xlist, p->xlist_count, cap_eff, st, p->sms,
                                &launches),
                "x headers");
         return PCDM_OK;
@@ -980,7 +1071,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
     // a grid that fits one cluster (<= 16 CTAs: small tau) synchronises with the hardware
     // cluster barrier instead of the global-memory grid barrier
-    Q.cluster_sync = (packed || bat_fallback) && packed_plan.ctas <= 16 ? cluster_sync : 0;
+    Q.cluster_sync = (packed || bat_fallback) && packed_plan.ctas <= 16 && !ragged_run ? cluster_sync : 0;
+    if (ragged_run) Q.pipeline = 0;
     // cache the hot rows when the hottest one is read >= 1024 times per iteration
     // (tau count_max / n); below that the per-iteration copy costs more than the
     // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;
@@ -1195,6 +1287,22 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                 nz_at = done + c;
                 nz_pending = true;
             }
+        } else if (packed && ragged_run) {
+            // the launch's slot arrays binned by column class (kernels_ragged.cu): by the
+            // presampler passes, or here
+            if (presample && ragged_plan) {
+                Q.bins = p->bins + done * tau;
+                Q.bcnt = p->bcnt + done * 8;
+            } else {
+                if ((s = ensure_bins(std::max(ichunk, c), std::max(ichunk, c))) != PCDM_OK) return s;
+                CK(bin_chunk(slots_c, tau, c, p->blk_off, p->blk_cls, p->bin_scr, p->bins, p->bcnt, st, p->sms, &launches),
+                   "binning");
+                Q.bins = p->bins;
+                Q.bcnt = p->bcnt;
+            }
+            Q.iters = c;
+            Q.k0 = done;
+            CK(launch_ragged(plan.ctas, Q, st, &launches), "ragged iteration kernel");
         } else if (packed) {
             Q.slots = slots_c;
             Q.iters = c;
@@ -1224,7 +1332,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                 // entries that became zero: it copies all of x
                 // (two passes: the list may name a column twice)
                 if ((s = x_out()) != PCDM_OK) return s;
-                CK(launch_xhdr_clear(p->blocks, p->packed_G, p->xlist, p->xlist_count, cap_eff, p->n, st, p->sms,
+                CK(launch_xhdr_clear(p->blocks, p->packed_G, p->blk_off, p->xlist, p->xlist_count, cap_eff, p->n, st, p->sms,
                                      &launches),
                    "x headers");
                 CK(cudaMemsetAsync(p->xlist_count, xdense ? 0xFF : 0, sizeof(unsigned long long), st), "memset x list");
@@ -1320,7 +1428,8 @@ pcdm_status pcdm_run_async(pcdm_problem* p, float* x, int64_t updates, int64_t t
     if (!p || !x) return fail(PCDM_EINVAL, "NULL argument");
     if (updates < 0 || tau_beta < 0) return fail(PCDM_EINVAL, "updates and tau_beta must be >= 0");
     if (!p->packed_G)
-        return fail(PCDM_EINVAL, "asynchronous variant needs max column length <= 62 (have %lld)", (long long)p->max_len);
+        return fail(PCDM_EINVAL, "asynchronous variant needs the uniform packed layout (max column length %lld)",
+                    (long long)p->max_len);
     if (p->loss != 0) return fail(PCDM_EINVAL, "asynchronous variant: LASSO problems only");
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");

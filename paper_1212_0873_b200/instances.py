@@ -42,6 +42,14 @@ class InstanceConfig:
     lam_frac: float = 0.1
     tau: int = 1
     iters: int = 1
+    # column lengths: "fixed" (nnz_per_col each) or "pareto": len = min(len_max,
+    # floor(len_min * U^(-1/alpha))), U uniform on (0, 1] -- a power-law (Zipf-tail)
+    # mix of short columns and a few very long ones, like the feature columns of the
+    # paper's KDDB data; nnz_per_col is then only the nominal mean
+    col_lengths: str = "fixed"
+    len_alpha: float = 1.5
+    len_min: int = 7
+    len_max: int = 10_000
 
 
 # BASELINE.json "configs", in order.
@@ -52,6 +60,16 @@ CONFIGS = {
                              tau=1 << 12, iters=10_000),
     "large": InstanceConfig("large", 2_000_000, 10_000_000, 20, 10_000, tau=65536, iters=2000),
     "huge": InstanceConfig("huge", 100_000_000, 500_000_000, 10, 100_000, tau=1 << 18, iters=500),
+}
+# Ragged column lengths (not a BASELINE.json config): the `large`
+# shape with power-law column lengths (Pareto alpha = 1.5 from 7, capped at 10^4
+# entries: mean ~20, ~190 columns at the cap), a stand-in for the KDDB-shaped
+# feature columns of PAPER.md:1388-1392.
+RAGGED_CONFIGS = {
+    "ragged": InstanceConfig("ragged", 2_000_000, 10_000_000, 20, 10_000, tau=65536, iters=2000,
+                             col_lengths="pareto"),
+    "ragged_small": InstanceConfig("ragged_small", 20_000, 6_000, 20, 200, tau=256, iters=400,
+                                   col_lengths="pareto", len_alpha=0.9, len_min=2, len_max=12_000),
 }
 SKEWED_TAUS = [1 << e for e in range(8, 17)]
 
@@ -116,8 +134,10 @@ def generate(cfg: InstanceConfig | str, seed: int = 0, device="cpu",
              chunk_cols: int = 1 << 23) -> Instance:
     """Build the instance of ``cfg`` (a name from CONFIGS or an InstanceConfig)."""
     if isinstance(cfg, str):
-        cfg = CONFIGS[cfg]
+        cfg = CONFIGS[cfg] if cfg in CONFIGS else RAGGED_CONFIGS[cfg]
     device = torch.device(device)
+    if cfg.col_lengths == "pareto":
+        return _generate_ragged(cfg, seed, device)
     m, n, c = cfg.m, cfg.n, cfg.nnz_per_col
     if not (1 <= c <= m):
         raise ValueError("need 1 <= nnz_per_col <= m")
@@ -163,6 +183,50 @@ def generate(cfg: InstanceConfig | str, seed: int = 0, device="cpu",
         atb = (val[sl].to(torch.float64) * bd[rowidx[sl].to(torch.int64)]).view(k, c).sum(1)
         amax = max(amax, float(atb.abs().max()))
     lam = cfg.lam_frac * amax
+    return Instance(cfg, m, n, colptr, rowidx, val, b, lam, xs_idx, xs_val.to(torch.float32))
+
+
+def _generate_ragged(cfg: InstanceConfig, seed: int, device) -> Instance:
+    """G1-G6 with power-law column lengths (cfg.col_lengths == "pareto"): lengths
+    drawn first, then each column's rows uniform and distinct (redraw duplicates),
+    sorted; values N(0,1); planted x*, b and lambda as for the fixed-length configs."""
+    m, n = cfg.m, cfg.n
+    if cfg.len_max > m:
+        raise ValueError("len_max must be <= m")
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    u = 1.0 - torch.rand(n, generator=gen, device=device, dtype=torch.float64)  # (0, 1]
+    lens = torch.floor(cfg.len_min * u.pow(-1.0 / cfg.len_alpha)).clamp_(max=cfg.len_max).to(torch.int64)
+    colptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    colptr[1:] = torch.cumsum(lens, 0)
+    nnz = int(colptr[-1])
+    col = torch.repeat_interleave(torch.arange(n, device=device), lens)
+    rows = torch.randint(0, m, (nnz,), generator=gen, device=device, dtype=torch.int64)
+    while True:
+        key = col * m + rows
+        key, _ = torch.sort(key)
+        rows = key - col * m  # col is sorted, so sorting the keys keeps each column's slice
+        dup = torch.zeros(nnz, dtype=torch.bool, device=device)
+        dup[1:] = key[1:] == key[:-1]
+        nd = int(dup.sum())
+        if nd == 0:
+            break
+        rows[dup] = torch.randint(0, m, (nd,), generator=gen, device=device, dtype=torch.int64)
+    rowidx = rows.to(torch.int32)
+    del rows, key
+    val = torch.randn(nnz, generator=gen, device=device, dtype=torch.float32)
+    s = min(cfg.s_star, n)
+    xs_idx = torch.sort(torch.randperm(n, generator=gen, device=device)[:s]).values
+    xs_val = torch.randn(s, generator=gen, device=device, dtype=torch.float64)
+    xfull = torch.zeros(n, dtype=torch.float64, device=device)
+    xfull[xs_idx] = xs_val
+    b64 = torch.zeros(m, dtype=torch.float64, device=device)
+    b64.index_add_(0, rowidx.to(torch.int64), val.to(torch.float64) * xfull[col])
+    b64 += cfg.noise * torch.randn(m, generator=gen, device=device, dtype=torch.float64)
+    b = b64.to(torch.float32)
+    atb = torch.zeros(n, dtype=torch.float64, device=device)
+    atb.index_add_(0, col, val.to(torch.float64) * b.to(torch.float64)[rowidx.to(torch.int64)])
+    lam = cfg.lam_frac * float(atb.abs().max())
     return Instance(cfg, m, n, colptr, rowidx, val, b, lam, xs_idx, xs_val.to(torch.float32))
 
 

@@ -136,7 +136,7 @@ def _ragged(m, n, lens, seed, lam_frac=0.1):
     return colptr, rowidx, val, b, I.lam_for(colptr, rowidx, val, b, lam_frac)
 
 
-@pytest.mark.parametrize("variant", ["smem", "block", "grid"])
+@pytest.mark.parametrize("variant", ["smem", "block", "grid", "packed", "auto"])
 def test_ragged_columns_with_empty_and_long(gpu, variant):
     m, n = 3000, 700
     rng = np.random.default_rng(1)
@@ -272,14 +272,19 @@ def test_packed_variant_both_barrier_schemes(gpu, monkeypatch, one_barrier, lens
                                    atol=1e-4 * np.max(np.abs(out["res"].r)))
 
 
-def test_packed_rejected_for_long_columns(gpu):
+def test_long_columns_take_the_ragged_layout(gpu):
+    # a column over 62 entries: the packed loop runs on the ragged layout (a CTA for the
+    # long column, sub-warps for the rest); the uniform-only loops are rejected
     c, r, v, b, lam = _ragged(300, 20, [100] + [3] * 19, 2)
     prob = pcdm.Problem(300, 20, c.to(gpu), r.to(gpu), v.to(gpu), b.to(gpu), lam)
+    prob.run(torch.zeros(20, device=gpu), 4, 1, variant="packed")
+    assert prob.stats()["lanes_per_column"] == 0
     with pytest.raises(pcdm.PCDMError) as e:
-        prob.run(torch.zeros(20, device=gpu), 4, 1, variant="packed")
+        prob.run(torch.zeros(20, device=gpu), 4, 1, variant="batched")
     assert e.value.status == pcdm.PCDM_EINVAL
-    prob.run(torch.zeros(20, device=gpu), 4, 1)  # AUTO falls back to a valid variant
+    prob.run(torch.zeros(20, device=gpu), 4, 1)  # AUTO
     prob.close()
+    assert_parity(run_both(c, r, v, b, lam, 300, 4, 50, seed=1, variant="packed"))
 
 
 # ------------------------------------------------------------------ many launches per run
