@@ -154,6 +154,10 @@ struct PackedParams {
                           //      global atomic per CTA and iteration (dense-step workloads)
     int hot_cache;        // 1: copy r_k[hot_rows] into shared memory every iteration (else
                           //    hot entries are gathered through the row table)
+    int bulk_stage;       // ragged layout: CTA-long column slices staged in shared memory by
+                          //    cp.async.bulk (TMA engine) pieces, scattered from the staged copy
+    int hot_stage;        // 1 (one-barrier scheme): scatters into hot rows accumulate in shared
+                          //    memory per CTA, one red.global.add per hot row and CTA per iteration
     // ragged layout (kernels_ragged.cu): per iteration the slots binned by class
     const int2* bins;     // [iters][tau] {i, chunk offset of column i}, grouped by class
     const int* bcnt;      // [iters][8] class starts (2, 4, 8, 16, 32 lanes, warp-long, CTA-long) and end
@@ -175,8 +179,8 @@ size_t bin_scratch_bytes(int64_t count);
 // slots [count][tau] -> bins [count][tau] {i, off[i]} grouped by class, bcnt [count][8]
 cudaError_t bin_chunk(const int* slots, int64_t tau, int64_t count, const long long* off, const unsigned char* cls,
                       int* scratch, int2* bins, int* bcnt, cudaStream_t st, int sms, int64_t* launches);
-size_t ragged_smem_bytes(int nhot);
-int ragged_ctas(int sms, bool logistic, int nhot);
+size_t ragged_smem_bytes(int nhot, bool bulk_stage);
+int ragged_ctas(int sms, bool logistic, int nhot, bool bulk_stage);
 cudaError_t launch_ragged(int ctas, const PackedParams& P, cudaStream_t st, int64_t* launches);
 // asynchronous variant (NEXT-4): no barriers, no sampler pass
 struct AsyncParams {
@@ -203,10 +207,11 @@ cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStrea
 // rows listed in hot_rows[0..nhot) (ascending) are stored as 0x80000000 | h
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
                         const int* hot_rows, int nhot, int4* blocks, cudaStream_t st, int sms, int64_t* launches);
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false, int nhot = 0, int list_cap = 0);
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false, int nhot = 0, int list_cap = 0,
+                bool hot_stage = false);
 cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
                           int64_t* launches);
-size_t packed_smem_bytes(int nhot, int list_cap = 0);
+size_t packed_smem_bytes(int nhot, int list_cap = 0, bool hot_stage = false);
 
 // ---- batched-snapshot loop (kernels_batched.cu): passes expand / sweep / steps / fold
 struct BatchedParams {

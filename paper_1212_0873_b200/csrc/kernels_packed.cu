@@ -84,6 +84,24 @@ __device__ __forceinline__ void scatter_chunk(float* r, const int4 c, int pair0,
     if (pair0 + 1 < len) red_add_f32(r + real_row(c.z, hrow), __int_as_float(c.w) * d);
 }
 
+// Scatter with the hot rows staged (P.hot_stage): contributions to a hot row go to the
+// CTA's shared-memory accumulator s_hacc[h] (shared atomics, no same-address L2
+// serialisation across the grid), flushed with one red.global.add per touched hot row
+// and CTA before the iteration's barrier; other rows as scatter_chunk.
+__device__ __forceinline__ void scatter_chunk_staged(float* r, const int4 c, int pair0, int len, float d,
+                                                     const int* hrow, float* s_hacc) {
+    if (pair0 < len) {
+        const float v = __int_as_float(c.y) * d;
+        if (c.x < 0) atomicAdd(s_hacc + (c.x & 0x7fffffff), v);
+        else red_add_f32(r + c.x, v);
+    }
+    if (pair0 + 1 < len) {
+        const float v = __int_as_float(c.w) * d;
+        if (c.z < 0) atomicAdd(s_hacc + (c.z & 0x7fffffff), v);
+        else red_add_f32(r + c.z, v);
+    }
+}
+
 // gathered r entry (hot rows from the shared-memory copy, or through the row table
 // when the run does not cache them)
 __device__ __forceinline__ float gather_r(const float* rP, int v, const float* s_hot, const int* s_hrow, bool cache) {
@@ -114,7 +132,12 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
     float* s_ld = (float*)(s_li + P.list_cap);
     int* s_lc = (int*)(s_ld + P.list_cap);
     int* s_lbase = s_lc + 1;
+    // staged hot-row scatters (P.hot_stage, one-barrier scheme): [nhot] accumulators
+    float* s_hacc = stage ? (float*)(s_lbase + 1) : (float*)(s_hrow + nhot);
+    const bool hstage = ONE_BARRIER && P.hot_stage && nhot > 0;
     if (stage && threadIdx.x == 0) *s_lc = 0;
+    if (hstage)
+        for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hacc[h] = 0.0f;
     const bool cache = P.hot_cache != 0;
     // CTAs without slots in an iteration skip the hot-row copy
     const bool has_slots = (int64_t)blockIdx.x * (blockDim.x / G) < tau;
@@ -152,7 +175,10 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
                 const float d = ld_l2_f32(P.nz_delta + prev * tau + e);
                 const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
                 const int len = __shfl_sync(gm, c.y, src);
-                if (t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+                if (t > 0) {
+                    if (hstage) scatter_chunk_staged(rQ, c, pair0, len, d, s_hrow, s_hacc);
+                    else scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+                }
             }
         }
         if (cache && has_slots) {
@@ -240,7 +266,21 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
             }
             if (ONE_BARRIER) {
                 d = __shfl_sync(gm, d, src);
-                if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+                if (d != 0.0f && t > 0) {
+                    if (hstage) scatter_chunk_staged(rQ, c, pair0, len, d, s_hrow, s_hacc);
+                    else scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+                }
+            }
+        }
+        if (hstage) {
+            // flush the CTA's hot-row sums into Q before the barrier publishes it
+            __syncthreads();
+            for (int h = threadIdx.x; h < nhot; h += blockDim.x) {
+                const float v = s_hacc[h];
+                if (v != 0.0f) {
+                    red_add_f32(rQ + s_hrow[h], v);
+                    s_hacc[h] = 0.0f;
+                }
             }
         }
         if (stage) {
@@ -439,7 +479,7 @@ cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
     const int tpb = (ONE && P.cluster_sync == 2) ? 1024 : kThreads;
     const void* fn = tpb == 1024 ? (const void*)pcdm_packed_kernel<G, ONE, LOG, 1024>
                                  : (const void*)pcdm_packed_kernel<G, ONE, LOG>;
-    const size_t smem = packed_smem_bytes(P.nhot, P.list_cap);
+    const size_t smem = packed_smem_bytes(P.nhot, P.list_cap, P.hot_stage != 0);
     if (P.cluster_sync) {  // the whole grid is one cluster (ctas <= 16)
         if (ctas > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
@@ -533,8 +573,9 @@ cudaError_t launch_gather_list(const float* x, const int* list, int64_t count, f
     return cudaGetLastError();
 }
 
-size_t packed_smem_bytes(int nhot, int list_cap) {
-    return (size_t)nhot * (sizeof(float) + sizeof(int)) + (list_cap > 0 ? (size_t)list_cap * 8 + 8 : 0);
+size_t packed_smem_bytes(int nhot, int list_cap, bool hot_stage) {
+    return (size_t)nhot * (sizeof(float) + sizeof(int)) + (list_cap > 0 ? (size_t)list_cap * 8 + 8 : 0) +
+           (hot_stage ? (size_t)nhot * sizeof(float) : 0);
 }
 
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
@@ -574,11 +615,11 @@ cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st,
     return cudaGetLastError();
 }
 
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot, int list_cap) {
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot, int list_cap, bool hot_stage) {
     int per_sm = 1;
     const void* fn = logistic ? (one_barrier ? kernel_ptr<true, true>(G) : kernel_ptr<false, true>(G))
                               : (one_barrier ? kernel_ptr<true, false>(G) : kernel_ptr<false, false>(G));
-    const size_t smem = packed_smem_bytes(nhot, list_cap);
+    const size_t smem = packed_smem_bytes(nhot, list_cap, hot_stage);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;

@@ -68,6 +68,34 @@ __device__ __forceinline__ int2 ld_stream_v2(const int2* p) {
     return v;
 }
 
+// ---- bulk (TMA engine) copies global -> shared with mbarrier completion (CTA-long columns)
+constexpr int kStageChunks = 2048;  // 32 KB of 16-byte chunks = 4096 entries per piece
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 template <int G>
 __device__ __forceinline__ unsigned gmask_of() {
     if constexpr (G == 32) {
@@ -242,7 +270,71 @@ __device__ __forceinline__ void ragged_long(const PackedParams& P, const int2* E
 #ifndef PCDM_RAGGED_MINB
 #define PCDM_RAGGED_MINB 3  // CTAs of 512 threads per SM (register cap 40)
 #endif
+// CTA-long columns with the column slice staged in shared memory by bulk copies
+// (P.bulk_stage): pieces of <= 4096 entries arrive through the TMA
+// engine (one cp.async.bulk per piece, completion on an mbarrier), the threads gather
+// from shared memory, and a column that fits one piece is scattered from the staged
+// copy instead of being read from global memory a second time.
 template <bool LOGISTIC>
+__device__ __forceinline__ void ragged_long_bulk(const PackedParams& P, const int2* E, int beg, int end, const float* rP,
+                                                 float* rQ, const float* s_hot, const int* s_hrow, bool cache, int cur,
+                                                 float* s_red, int4* s_stage, unsigned long long* bar,
+                                                 unsigned& phase) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int q = beg + blockIdx.x; q < end; q += gridDim.x) {
+        const int2 e = ld_stream_v2(E + q);
+        const int4* blk = P.blocks + (unsigned)e.y;
+        const int len = ld_l2_v4(blk).y;
+        const int npair = (len + 1) / 2;
+        float acc = 0.0f;
+        for (int base = 0; base < npair; base += kStageChunks) {
+            const int cnt = min(kStageChunks, npair - base);
+            if (threadIdx.x == 0) {
+                // the generic-proxy reads of the previous piece (ordered by the __syncthreads
+                // below) come before the async-proxy write of this one
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar, (unsigned)cnt * 16u);
+                bulk_g2s(s_stage, blk + 1 + base, (unsigned)cnt * 16u, bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+                const int4 c = s_stage[t];
+                const int p0 = 2 * (base + t);
+                const float ra = grad_weight<LOGISTIC>(gather_r(rP, c.x, s_hot, s_hrow, cache));
+                const float rb = p0 + 1 < len ? grad_weight<LOGISTIC>(gather_r(rP, c.z, s_hot, s_hrow, cache)) : 0.0f;
+                acc += fmaf(__int_as_float(c.y), ra, __int_as_float(c.w) * rb);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) s_red[warp] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float g = 0.0f;
+            for (int w = 0; w < nwarps; ++w) g += s_red[w];
+            const int4 h = ld_l2_v4(blk);
+            const float xi = P.xlist ? __int_as_float(h.z) : ld_l2_f32(P.x + e.x);
+            const float xp = block_step<LOGISTIC>(xi, g, P.beta * __int_as_float(h.x), P.lambda);
+            const float d = xp - xi;
+            if (d != 0.0f) record_step<LOGISTIC>(P, e.x, (unsigned)e.y, xp, d, cur);
+            s_red[32] = d;
+        }
+        __syncthreads();
+        const float d = s_red[32];
+        if (d != 0.0f) {
+            if (npair <= kStageChunks)  // the whole slice is still staged
+                for (int t = threadIdx.x; t < npair; t += blockDim.x) scatter_chunk(rQ, s_stage[t], 2 * t, len, d, s_hrow);
+            else
+                for (int t = 1 + threadIdx.x; t <= npair; t += blockDim.x)
+                    scatter_chunk(rQ, ld_stream_v4(blk + t), 2 * (t - 1), len, d, s_hrow);
+        }
+        __syncthreads();  // s_red and s_stage reused by the next long column
+    }
+}
+
+template <bool LOGISTIC, bool BULK>
 __global__ void __launch_bounds__(kThreads, PCDM_RAGGED_MINB) pcdm_ragged_kernel(PackedParams P) {
     unsigned bar_target = 0;
     extern __shared__ float s_dyn[];
@@ -251,9 +343,18 @@ __global__ void __launch_bounds__(kThreads, PCDM_RAGGED_MINB) pcdm_ragged_kernel
     int* s_hrow = (int*)(s_dyn + nhot);    // [nhot] hot row ids
     float* s_red = (float*)(s_hrow + nhot);  // [33] block reduction + the long column's step
     int* s_cb = (int*)(s_red + 33);          // [2][8] class bounds of this / the next iteration
+    // P.bulk_stage: [kStageChunks] staged column slice (16-byte aligned) + its mbarrier
+    int4* s_stage = (int4*)(((uintptr_t)(s_cb + 16) + 15) & ~(uintptr_t)15);
+    unsigned long long* s_bar = (unsigned long long*)(s_stage + kStageChunks);
+    unsigned phase = 0;
+    constexpr bool bulk = BULK;
     const bool cache = P.hot_cache != 0;
     for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
     if (threadIdx.x < 8 && P.iters > 0) s_cb[threadIdx.x] = ld_stream_s32(P.bcnt + threadIdx.x);
+    if (bulk && threadIdx.x == 0) {
+        mbar_init(s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -280,7 +381,11 @@ __global__ void __launch_bounds__(kThreads, PCDM_RAGGED_MINB) pcdm_ragged_kernel
         }
         const int2* E = P.bins + it * P.tau;
         const int* cb = s_cb + (it & 1) * 8;  // class starts [0..6], end [7] (loaded before the barrier)
-        ragged_long<LOGISTIC>(P, E, cb[6], cb[7], rP, rQ, s_hot, s_hrow, cache, cur, s_red);
+        if constexpr (bulk)
+            ragged_long_bulk<LOGISTIC>(P, E, cb[6], cb[7], rP, rQ, s_hot, s_hrow, cache, cur, s_red, s_stage, s_bar,
+                                       phase);
+        else
+            ragged_long<LOGISTIC>(P, E, cb[6], cb[7], rP, rQ, s_hot, s_hrow, cache, cur, s_red);
         ragged_warp<LOGISTIC>(P, E, cb[5], cb[6], rP, rQ, s_hot, s_hrow, cache, cur);
         ragged_class<32, LOGISTIC>(P, E, cb[4], cb[5], rP, rQ, s_hot, s_hrow, cache, cur);
         ragged_class<16, LOGISTIC>(P, E, cb[3], cb[4], rP, rQ, s_hot, s_hrow, cache, cur);
@@ -488,11 +593,19 @@ cudaError_t bin_chunk(const int* slots, int64_t tau, int64_t count, const long l
     return cudaGetLastError();
 }
 
-size_t ragged_smem_bytes(int nhot) { return (size_t)nhot * (sizeof(float) + sizeof(int)) + (33 + 16) * sizeof(float); }
+size_t ragged_smem_bytes(int nhot, bool bulk_stage) {
+    return (size_t)nhot * (sizeof(float) + sizeof(int)) + (33 + 16) * sizeof(float) +
+           (bulk_stage ? 16 + (size_t)kStageChunks * 16 + 8 : 0);
+}
 
-int ragged_ctas(int sms, bool logistic, int nhot) {
-    const void* fn = logistic ? (const void*)pcdm_ragged_kernel<true> : (const void*)pcdm_ragged_kernel<false>;
-    const size_t smem = ragged_smem_bytes(nhot);
+static const void* ragged_fn(bool logistic, bool bulk) {
+    if (bulk) return logistic ? (const void*)pcdm_ragged_kernel<true, true> : (const void*)pcdm_ragged_kernel<false, true>;
+    return logistic ? (const void*)pcdm_ragged_kernel<true, false> : (const void*)pcdm_ragged_kernel<false, false>;
+}
+
+int ragged_ctas(int sms, bool logistic, int nhot, bool bulk_stage) {
+    const void* fn = ragged_fn(logistic, bulk_stage);
+    const size_t smem = ragged_smem_bytes(nhot, bulk_stage);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
@@ -503,8 +616,9 @@ int ragged_ctas(int sms, bool logistic, int nhot) {
 cudaError_t launch_ragged(int ctas, const PackedParams& P, cudaStream_t st, int64_t* launches) {
     ++*launches;
     void* args[] = {(void*)&P};
-    const void* fn = P.logistic ? (const void*)pcdm_ragged_kernel<true> : (const void*)pcdm_ragged_kernel<false>;
-    return cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kThreads), args, ragged_smem_bytes(P.nhot), st);
+    const void* fn = ragged_fn(P.logistic != 0, P.bulk_stage != 0);
+    return cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kThreads), args,
+                                       ragged_smem_bytes(P.nhot, P.bulk_stage != 0), st);
 }
 
 }  // namespace pcdm_internal

@@ -889,6 +889,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (clustered) packed = false;
     bool one_barrier = false;
     int list_cap = 0;
+    bool hot_stage = false;
+    bool bulk_stage = false;
     int cluster_sync = 0;
     const bool ragged_run = packed && p->ragged;
     if (ragged_run) {
@@ -906,14 +908,18 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.variant = PCDM_VARIANT_PACKED;
         plan.lanes = 0;  // per column: 2..32 lanes, or a CTA beyond 62 entries
         plan.threads = 512;
-        plan.ctas = ragged_ctas(p->sms, p->loss == 1, p->nhot);
+        // CTA-long column slices staged in shared memory by bulk copies (SURVEY 8 row X2,
+        // profiles/r02_bulk_stage_ab.jsonl); PCDM_BULK_STAGE=0/1 overrides
+        const char* bs_env = getenv("PCDM_BULK_STAGE");
+        bulk_stage = bs_env ? atoi(bs_env) != 0 : false;
+        plan.ctas = ragged_ctas(p->sms, p->loss == 1, p->nhot, bulk_stage);
         // small tau: only about as many CTAs as the average column needs lanes
         const double gavg = (double)p->ragged_chunks / (double)p->n;
         const int64_t busy = std::max<int64_t>(1, (int64_t)ceil((double)tau * gavg / plan.threads));
         if (busy < plan.ctas) plan.ctas = (int)busy;
         if (const char* cs = getenv("PCDM_CTAS")) {
             const int v = atoi(cs);
-            if (v >= 1) plan.ctas = std::min(v, ragged_ctas(p->sms, p->loss == 1, p->nhot));
+            if (v >= 1) plan.ctas = std::min(v, ragged_ctas(p->sms, p->loss == 1, p->nhot, bulk_stage));
         }
     } else if (packed) {
         // one barrier per iteration (double-buffered r, the previous iteration's steps
@@ -928,10 +934,17 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             p->r2 = nullptr;
             one_barrier = false;
         }
+        // hot-row scatters staged in shared memory per CTA (one-barrier scheme; SURVEY 8
+        // row X2, profiles/r02_hot_stage_ab.jsonl); PCDM_HOT_STAGE=0/1 overrides
+        const char* hs_env = getenv("PCDM_HOT_STAGE");
+        // default: dense-step workloads (logistic: every visited coordinate steps) -- skewed,
+        // logistic tau = 2^16: 498 -> 31 ms of iteration kernel per 1000 iterations; LASSO's
+        // sparse steps lose (169 -> 176 ms per 1e4 iterations: the per-iteration flush costs more)
+        hot_stage = one_barrier && p->nhot > 0 && (hs_env ? atoi(hs_env) != 0 : p->loss == 1);
         plan.variant = PCDM_VARIANT_PACKED;
         plan.lanes = p->packed_G;
         plan.threads = 512;
-        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot);
+        plan.ctas = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, 0, hot_stage);
         // small tau: only CTAs that own slots; the others would only add arrivals to
         // every grid barrier (PCDM_CTAS overrides, for measurements)
         const int64_t busy = (tau * p->packed_G + plan.threads - 1) / plan.threads;
@@ -951,7 +964,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         }
         if (const char* cs = getenv("PCDM_CTAS")) {
             const int v = atoi(cs);
-            if (v >= 1) plan.ctas = std::min(v, packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot));
+            if (v >= 1)
+                plan.ctas = std::min(v, packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, 0, hot_stage));
         }
         // dense-step workloads (logistic: every step is nonzero): stage each CTA's steps in
         // shared memory, one atomic on the list counter per CTA instead of one per step
@@ -960,9 +974,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         if (sl ? atoi(sl) != 0 : p->loss == 1) {
             const int64_t groups = (int64_t)plan.ctas * plan.threads / p->packed_G;
             const int64_t cap = ((tau + groups - 1) / groups) * (plan.threads / p->packed_G);
-            const int full = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot);
+            const int full = packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, 0, hot_stage);
             if (cap * 8 <= 32 * 1024 &&
-                packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, (int)cap) == full)
+                packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, (int)cap, hot_stage) == full)
                 list_cap = (int)cap;
         }
     }
@@ -1060,6 +1074,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.hot_rows = p->hot_rows;
     Q.nhot = p->nhot;
     Q.list_cap = list_cap;
+    Q.hot_stage = hot_stage ? 1 : 0;
+    Q.bulk_stage = ragged_run && bulk_stage ? 1 : 0;
     // software-pipelined slots when r is L2-resident (the loop is latency-bound there:
     // large 26.1 -> 25.8, skewed tau=2^16 163 -> 158 ms/step); for r much larger than L2
     // (huge) the extra loads in flight cost more than they hide (29.0 -> 29.4 ms)

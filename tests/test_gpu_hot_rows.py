@@ -52,11 +52,14 @@ def test_hot_row_selection(gpu, zipf, monkeypatch):
     assert _hot_count(zipf, gpu, tau=(1024 * zipf.n + top - 1) // top) == want
 
 
+@pytest.mark.parametrize("stage", ["0", "1"], ids=["scatter-global", "scatter-staged"])
 @pytest.mark.parametrize("one_barrier", ["1", "0"])
 @pytest.mark.parametrize("hot_max,cache", [(None, "1"), ("5", "1"), (None, "0")])
-def test_hot_rows_parity(gpu, zipf, monkeypatch, one_barrier, hot_max, cache):
+def test_hot_rows_parity(gpu, zipf, monkeypatch, one_barrier, hot_max, cache, stage):
+    # stage: hot-row scatters accumulated per CTA in shared memory (one-barrier scheme)
     monkeypatch.setenv("PCDM_ONE_BARRIER", one_barrier)
     monkeypatch.setenv("PCDM_HOT_CACHE", cache)
+    monkeypatch.setenv("PCDM_HOT_STAGE", stage)
     if hot_max:
         monkeypatch.setenv("PCDM_HOT_MAX", hot_max)
     inst = zipf
@@ -72,7 +75,10 @@ def test_hot_rows_parity(gpu, zipf, monkeypatch, one_barrier, hot_max, cache):
     assert_parity(out)
 
 
-def test_hot_rows_logistic(gpu, zipf):
+@pytest.mark.parametrize("stage", ["0", "1"], ids=["scatter-global", "scatter-staged"])
+def test_hot_rows_logistic(gpu, zipf, monkeypatch, stage):
+    # logistic: every visited coordinate steps, so every iteration scatters into the hot rows
+    monkeypatch.setenv("PCDM_HOT_STAGE", stage)
     y = _labels(zipf.m, 3)
     out = run_both_logistic(zipf.colptr, zipf.rowidx, zipf.val, y, 1.0, zipf.m, 2048, 100, variant="packed")
     assert out["st"]["hot_rows"] > 0

@@ -37,8 +37,12 @@ def zipf_cols():
     return inst
 
 
+@pytest.mark.parametrize("bulk", ["0", "1"], ids=["ld-global", "bulk-staged"])
 @pytest.mark.parametrize("variant", ["auto", "packed"])
-def test_ragged_power_law_columns(gpu, zipf_cols, variant):
+def test_ragged_power_law_columns(gpu, zipf_cols, monkeypatch, variant, bulk):
+    # bulk: CTA-long column slices staged in shared memory by cp.async.bulk (pieces of 4096
+    # entries; the 12000-entry column takes three)
+    monkeypatch.setenv("PCDM_BULK_STAGE", bulk)
     inst = zipf_cols
     x0 = np.random.default_rng(2).normal(size=inst.n) * (np.arange(inst.n) % 9 == 0)
     for tau, iters, refresh in ((1, 400, 0), (16, 300, 0), (256, 400, 0), (2000, 30, 5), (inst.n, 6, -1)):
@@ -58,16 +62,19 @@ def test_ragged_config_from_zero(gpu, zipf_cols):
     assert out["stats"]["nonzero_deltas"] > 0
 
 
+@pytest.mark.parametrize("bulk", ["0", "1"], ids=["ld-global", "bulk-staged"])
 @pytest.mark.parametrize("lens_kind", ["uniform10", "mixed", "one_long"])
-def test_forced_ragged_layout(gpu, monkeypatch, lens_kind):
+def test_forced_ragged_layout(gpu, monkeypatch, lens_kind, bulk):
     # PCDM_LAYOUT=ragged (read at create) on matrices the uniform layout would take
     monkeypatch.setenv("PCDM_LAYOUT", "ragged")
-    m, n = 5000, 3000
+    monkeypatch.setenv("PCDM_BULK_STAGE", bulk)
+    m, n = 9000, 3000
     rng = np.random.default_rng(5)
     lens = {"uniform10": np.full(n, 10), "mixed": rng.integers(0, 70, size=n),
             "one_long": np.full(n, 3)}[lens_kind]
     lens[:4] = 0
     if lens_kind == "one_long":
+        lens[16] = 4096 * 2 + 1  # CTA-long: three bulk pieces, the last one entry
         lens[17] = 4999
         lens[18] = 63
         lens[19] = 62
