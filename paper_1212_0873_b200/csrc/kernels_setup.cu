@@ -7,6 +7,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -41,33 +43,124 @@ __global__ void hot_candidates_kernel(int64_t m, const int* __restrict__ counts,
     }
 }
 
-// One warp per column: colptr monotone, rows in [0,m) and strictly increasing,
-// values finite.
-__global__ void validate_kernel(int64_t m, int64_t n, int64_t nnz, const long long* __restrict__ colptr,
-                                const int* __restrict__ rowidx, const float* __restrict__ val,
-                                int* __restrict__ flags) {
+// Column tiles: a warp takes 32 consecutive columns and walks their entries
+// [colptr[i0], colptr[i0 + 32]) with all lanes, coalesced (a warp per column leaves 22
+// of 32 lanes idle on 10-entry columns and is latency-bound).  tile_bounds loads the 33
+// boundaries (lane l holds b_l = colptr[i0 + l], lane 0 also b_32 in *b32);
+// tile_col finds the tile-local column of entry p: the largest k with b_k <= p.
+__device__ __forceinline__ long long tile_bounds(const long long* __restrict__ colptr, int64_t n, int64_t i0,
+                                                 long long* b32) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = i0 + lane;
+    const long long b = colptr[i < n ? i : n];
+    *b32 = colptr[i0 + 32 < n ? i0 + 32 : n];
+    return b;
+}
+__device__ __forceinline__ int tile_col(long long p, long long b) {
+    int k = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const long long bk = __shfl_sync(0xffffffffu, b, k + step);
+        if (bk <= p) k += step;
+    }
+    return k;
+}
+
+// CSC validation on column tiles: colptr monotone and within [0, nnz], rows in [0, m)
+// and strictly increasing within a column, values finite.
+__global__ void validate_tile_kernel(int64_t m, int64_t n, int64_t nnz, const long long* __restrict__ colptr,
+                                     const int* __restrict__ rowidx, const float* __restrict__ val,
+                                     int* __restrict__ flags) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     int bad = 0;
-    if (warp == 0 && lane == 0) {
-        if (colptr[0] != 0 || colptr[n] != nnz) bad |= FLAG_BAD_COLPTR;
-    }
-    for (int64_t i = warp; i < n; i += nwarps) {
-        const long long s = colptr[i], e = colptr[i + 1];
-        if (e < s || s < 0 || e > nnz) {
+    if (warp == 0 && lane == 0 && (colptr[0] != 0 || colptr[n] != nnz)) bad |= FLAG_BAD_COLPTR;
+    for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
+        long long e32;
+        const long long b = tile_bounds(colptr, n, i0, &e32);
+        const long long bn = __shfl_down_sync(0xffffffffu, b, 1);
+        const long long next = lane == 31 ? e32 : bn;
+        const bool col_ok = next >= b && b >= 0 && next <= nnz;
+        if (!__all_sync(0xffffffffu, col_ok)) {
             bad |= FLAG_BAD_COLPTR;
             continue;
         }
-        for (long long p = s + lane; p < e; p += 32) {
-            const int r = rowidx[p];
-            if (r < 0 || (int64_t)r >= m) bad |= FLAG_BAD_ROW;
-            if (p > s && rowidx[p - 1] >= r) bad |= FLAG_ROW_ORDER;
-            if (!isfinite(val[p])) bad |= FLAG_NONFINITE_VAL;
+        const long long s = __shfl_sync(0xffffffffu, b, 0);
+        for (long long p0 = s; p0 < e32; p0 += 32) {  // all lanes (tile_col shuffles)
+            const long long p = p0 + lane;
+            const int k = tile_col(p, b);
+            const bool start = __shfl_sync(0xffffffffu, b, k) == p;  // first entry of its column
+            if (p < e32) {
+                const int r = rowidx[p];
+                if (r < 0 || (int64_t)r >= m) bad |= FLAG_BAD_ROW;
+                if (!start && rowidx[p - 1] >= r) bad |= FLAG_ROW_ORDER;
+                if (!isfinite(val[p])) bad |= FLAG_NONFINITE_VAL;
+            }
         }
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (lane == 0 && bad) atomicOr(flags, bad);
+}
+
+// L_i = sum_p val_p^2 on column tiles: fp64 segmented warp sums (entries of a column are
+// consecutive lanes), one fp64 accumulator per tile column in shared memory.
+__global__ void col_norms_tile_kernel(int64_t n, const long long* __restrict__ colptr, const float* __restrict__ val,
+                                      float* __restrict__ L) {
+    __shared__ double s_acc[kThreads];
+    const int lane = threadIdx.x & 31;
+    double* acc = s_acc + (threadIdx.x & ~31);
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
+        long long e32;
+        const long long b = tile_bounds(colptr, n, i0, &e32);
+        acc[lane] = 0.0;
+        __syncwarp();
+        const long long s = __shfl_sync(0xffffffffu, b, 0);
+        for (long long p0 = s; p0 < e32; p0 += 32) {
+            const long long p = p0 + lane;
+            const bool valid = p < e32;
+            const double v = valid ? (double)ld_stream_f32(val + p) : 0.0;
+            const int kt = tile_col(p, b);  // all lanes (shuffles)
+            const int k = valid ? kt : 32;
+            double sum = v * v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan (keys non-decreasing)
+                const double y = __shfl_up_sync(0xffffffffu, sum, o);
+                const int ky = __shfl_up_sync(0xffffffffu, k, o);
+                if (lane >= o && ky == k) sum += y;
+            }
+            const int kn = __shfl_down_sync(0xffffffffu, k, 1);
+            if (valid && (lane == 31 || kn != k)) acc[k] += sum;  // the segment's last lane
+            __syncwarp();
+        }
+        if (i0 + lane < n) L[i0 + lane] = (float)acc[lane];
+        __syncwarp();
+    }
+}
+
+// counts[row]++ restricted to rows in [lo, hi): the row range's counters stay in L2
+// while every pass streams the whole row-index array (16-byte loads).
+__global__ void row_counts_range_kernel(int64_t nnz, const int* __restrict__ rowidx, int lo, int hi,
+                                        int* __restrict__ counts) {
+    const int64_t nv = nnz / 4;
+    const int4* r4 = (const int4*)rowidx;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nv; q += (int64_t)gridDim.x * blockDim.x) {
+        int4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(r4 + q));
+        if (v.x >= lo && v.x < hi) atomicAdd(counts + v.x, 1);
+        if (v.y >= lo && v.y < hi) atomicAdd(counts + v.y, 1);
+        if (v.z >= lo && v.z < hi) atomicAdd(counts + v.z, 1);
+        if (v.w >= lo && v.w < hi) atomicAdd(counts + v.w, 1);
+    }
+    for (int64_t p = nv * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int r = rowidx[p];
+        if (r >= lo && r < hi) atomicAdd(counts + r, 1);
+    }
 }
 
 __global__ void check_finite_kernel(int64_t count, const float* __restrict__ v, int flag_bit,
@@ -99,25 +192,6 @@ __global__ void max_kernel(int64_t count, const int* __restrict__ v, int* __rest
         best = max(best, v[t]);
     best = __reduce_max_sync(0xffffffffu, best);
     if ((threadIdx.x & 31) == 0) atomicMax(out, best);
-}
-
-// L_i = sum_p val_p^2, fp64 accumulation, one warp per column (lanes stride).
-__global__ void col_norms_kernel(int64_t n, const long long* __restrict__ colptr,
-                                 const float* __restrict__ val, float* __restrict__ L) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        const long long s = colptr[i], e = colptr[i + 1];
-        double acc = 0.0;
-        for (long long p = s + lane; p < e; p += 32) {
-            const double v = (double)ld_stream_f32(val + p);
-            acc += v * v;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) L[i] = (float)acc;
-    }
 }
 
 __global__ void neg_b_kernel(int64_t m, const float* __restrict__ b, double* __restrict__ r64) {
@@ -334,9 +408,9 @@ cudaError_t launch_objective_logistic(int64_t m, int64_t n, const double* s64, c
 
 
 cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches) {
-    const int blocks = grid_for(A.n * 32, kThreads, sms * 16);
-    validate_kernel<<<blocks, kThreads, 0, st>>>(A.m, A.n, A.nnz, (const long long*)A.colptr, A.rowidx,
-                                                 A.val, flags);
+    const int blocks = grid_for(A.n, kThreads, sms * 16);  // a warp per 32-column tile
+    validate_tile_kernel<<<blocks, kThreads, 0, st>>>(A.m, A.n, A.nnz, (const long long*)A.colptr, A.rowidx,
+                                                      A.val, flags);
     ++*launches;
     return cudaGetLastError();
 }
@@ -352,9 +426,21 @@ cudaError_t launch_check_finite(int64_t count, const float* v, int flag_bit, int
 cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int sms, int64_t* launches) {
     cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)A.m, st);
     if (e != cudaSuccess) return e;
-    const int blocks = grid_for(A.nnz, kThreads, sms * 16);
-    row_counts_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, counts);
-    ++*launches;
+    // counters of at most 2^24 rows (64 MB) per pass stay in L2 (huge: 189 -> see
+    // profiles/r02_create_ab.jsonl); small m: one pass with warp-aggregated atomics
+    const int64_t tile = (int64_t)1 << 24;
+    if (A.m <= tile) {
+        const int blocks = grid_for(A.nnz, kThreads, sms * 16);
+        row_counts_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, counts);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    const int blocks = grid_for(A.nnz / 4 + 1, kThreads, sms * 8);
+    for (int64_t lo = 0; lo < A.m; lo += tile) {
+        row_counts_range_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, (int)lo, (int)std::min(A.m, lo + tile),
+                                                             counts);
+        ++*launches;
+    }
     return cudaGetLastError();
 }
 
@@ -378,8 +464,8 @@ cudaError_t launch_max(int64_t count, const int* v, int* out, cudaStream_t st, i
 }
 
 cudaError_t launch_col_norms(const DevCSC& A, float* L, cudaStream_t st, int sms, int64_t* launches) {
-    const int blocks = grid_for(A.n * 32, kThreads, sms * 16);
-    col_norms_kernel<<<blocks, kThreads, 0, st>>>(A.n, (const long long*)A.colptr, A.val, L);
+    const int blocks = grid_for(A.n, kThreads, sms * 16);  // a warp per 32-column tile
+    col_norms_tile_kernel<<<blocks, kThreads, 0, st>>>(A.n, (const long long*)A.colptr, A.val, L);
     ++*launches;
     return cudaGetLastError();
 }
