@@ -39,9 +39,9 @@ from paper_1212_0873_b200 import instances as I  # noqa: E402
 
 METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline) at 1 B200"
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
-VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", 6: "cluster", -1: "async"}
+VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", -1: "async"}
 KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
-                     5: "batch_expand+batch_sweep+pcdm_batched_slot+batch_fold", 6: "pcdm_cluster_kernel",
+                     5: "batch_expand+batch_sweep+pcdm_batched_slot+batch_fold",
                      -1: "pcdm_async_kernel"}
 # The oracle timing sample, per config (one definition for the cpu_baseline of our
 # arm and for every step of --impl reference): iterations k = 0..K'-1 of the

@@ -62,13 +62,18 @@ typedef enum {
                              BATCHED for LASSO when 4m > 2 x L2 and E|S| >= 2^17 and
                              E|S| >= 0.8 tau (handing the rest of the run to PACKED if
                              its steps turn out dense); PACKED
-                             otherwise when max column length <= 62; GRID beyond    */
+                             otherwise; GRID when no packed copy of A fits in memory */
     PCDM_VARIANT_GRID = 1, /* persistent cooperative grid, r in HBM/L2, grid barriers    */
     PCDM_VARIANT_SMEM = 2, /* one CTA, A, r, x, L resident in shared memory (small A)    */
     PCDM_VARIANT_BLOCK = 3, /* one CTA, data in HBM/L2, __syncthreads barriers           */
     PCDM_VARIANT_PACKED = 4, /* persistent grid on packed column blocks (one coalesced line
                                per column); one barrier per iteration with double-buffered
-                               r (PCDM_ONE_BARRIER=0: two).  Needs max column length <= 62 */
+                               r.  Uniform layout (every column G lanes, G from the longest
+                               column <= 62 entries) or, chosen at create when a column is
+                               longer than 62 entries or would double every column's lanes,
+                               the ragged layout: per sampled column 2..32 lanes, a warp
+                               (63..1024 entries) or a CTA (longer) by its length, the
+                               slots binned by class after the sampler */
     PCDM_VARIANT_BATCHED = 5, /* packed blocks; per chunk of iterations the partial
                                derivatives a_i^T r_0 of all sampled columns are computed at
                                once from the chunk's starting residual (gathers sorted by
@@ -76,14 +81,7 @@ typedef enum {
                                a_i^T (r_k - r_0) on the rows the chunk's steps touched.
                                Same iteration (alg:PCD1), different summation order of g_i.
                                For r much larger than L2 and sparse steps (LASSO).  Needs
-                               max column length <= 62 */
-    PCDM_VARIANT_CLUSTER = 6 /* packed blocks; r split over the shared memories of one
-                               thread-block cluster (<= 16 CTAs), gathers and scatters in
-                               distributed shared memory, two hardware cluster barriers per
-                               iteration.  Needs 4m bytes / cluster size to fit in shared
-                               memory (m <= ~900K) and max column length <= 62.  Measured
-                               slower than PACKED on medium; AUTO picks it only with
-                               PCDM_CLUSTER=1 */
+                               the uniform packed layout */
 } pcdm_variant;
 
 /* Doubly uniform samplings (tbl:ESO PAPER.md:324-355).  A run
@@ -127,7 +125,8 @@ typedef struct {
     int32_t variant;            /* pcdm_variant actually used                       */
     int32_t grid_ctas;          /* CTAs of the iteration kernel                     */
     int32_t threads_per_cta;
-    int32_t lanes_per_column;   /* threads cooperating on one sampled column        */
+    int32_t lanes_per_column;   /* threads cooperating on one sampled column (0: chosen
+                                   per column, the ragged packed layout)              */
     int64_t chunk_iters;        /* iterations per iteration-kernel launch (max)     */
     int64_t iter_launches;      /* launches of the iteration kernel                 */
     double iter_kernel_ms;      /* summed device time of the iteration kernel       */

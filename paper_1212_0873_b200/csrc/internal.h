@@ -5,6 +5,12 @@
 
 namespace pcdm_internal {
 
+// Tuning and test knobs (A/B measurements, forced layouts / loops in tests) are
+// environment variables read ONLY when PCDM_DEBUG_KNOBS=1, on every call (no
+// process-wide caching); any other process runs the measured defaults whatever its
+// environment holds.  Returns the variable's value or nullptr.
+const char* knob(const char* name);
+
 struct DevCSC {
     int64_t m, n, nnz;
     const int64_t* colptr;  // device int64[n+1]
@@ -251,31 +257,7 @@ int batched_rb(int cq_log);
 int batched_ctas(int G, int sms, bool logistic, int nhot);
 cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches);
 
-// ---- cluster-resident loop (kernels_cluster.cu): r in one cluster's distributed shared memory
-struct ClusterParams {
-    int4* blocks;         // packed column blocks
-    const int* slots;     // [iters][tau]
-    int64_t tau;
-    int64_t iters;
-    float beta;
-    float lambda;
-    float* r;             // residual (margins): loaded at launch start, written back at the end
-    int64_t m;
-    int rpc;              // rows per CTA (cluster size x rpc >= m)
-    float* x;
-    int* xlist;
-    unsigned long long* xlist_count;
-    int64_t xlist_cap;
-    const int* hot_rows;
-    int nhot;
-    int list_cap;         // per-CTA step list capacity (>= slots a CTA handles per iteration)
-    int* flags;
-    unsigned long long* nz_total;
-    int logistic;
-};
-size_t cluster_smem_bytes(int rpc, int nhot, int list_cap);
-int cluster_plan(int G, bool logistic, size_t smem, int want);
-cudaError_t launch_cluster(int G, int cs, const ClusterParams& P, size_t smem, cudaStream_t st, int64_t* launches);
+
 
 // Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
 IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,

@@ -610,8 +610,8 @@ __global__ void batch_fold_kernel(BatchedParams P) {
 template <int G>
 const void* step_kernel(bool logistic) {
     if constexpr (G <= 8) {
-        static const bool group = [] {
-            const char* v = getenv("PCDM_BATCHED_GROUP");
+        const bool group = [] {
+            const char* v = knob("PCDM_BATCHED_GROUP");
             return v && atoi(v) != 0;
         }();
         if (!group)

@@ -304,7 +304,7 @@ IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau
     if (variant == 2) {
         L.ctas = 1;
         L.lanes = pow2_clamp(avg, 1, 32);
-        if (const char* sl = getenv("PCDM_SMEM_LANES")) L.lanes = pow2_clamp(atoi(sl), 1, 32);  // A/B
+        if (const char* sl = knob("PCDM_SMEM_LANES")) L.lanes = pow2_clamp(atoi(sl), 1, 32);  // A/B
         // as many threads as the slots need (each __syncthreads waits for all of them)
         L.threads = std::max(64, std::min(kSmemThreads, pow2_clamp(tau * L.lanes, 64, kSmemThreads)));
         L.smem = sm;

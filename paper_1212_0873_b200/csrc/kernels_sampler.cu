@@ -380,21 +380,21 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
         // CAS straight on the home entry (the tables were just cleared): huge sampler
         // 8.23 -> 7.05 ms/step, large 8.80 -> 7.68 (profiles/r01_sampler_cas_first_ab.jsonl);
         // PCDM_CAS_FIRST=0 restores load-then-CAS
-        static const bool cas_first = [] {
-            const char* v = getenv("PCDM_CAS_FIRST");
+        const bool cas_first = [] {
+            const char* v = knob("PCDM_CAS_FIRST");
             return !(v && atoi(v) == 0);
         }();
         // round 0 records where each value landed, so the check pass reads that entry
         // instead of probing (huge sampler 7.57 -> 6.03 ms/step,
         // profiles/r01_sampler_check_at_ab.jsonl); PCDM_CHECK_AT=0 probes
-        static const bool rec_at = [] {
-            const char* v = getenv("PCDM_CHECK_AT");
+        const bool rec_at = [] {
+            const char* v = knob("PCDM_CHECK_AT");
             return !(v && atoi(v) == 0);
         }();
         // contest mode (default with CAS-first): duplicates recorded at insert time, no
         // check pass over all slots (PCDM_CONTEST=0: check pass)
-        static const bool contest = [] {
-            const char* v = getenv("PCDM_CONTEST");
+        const bool contest = [] {
+            const char* v = knob("PCDM_CONTEST");
             return !(v && atoi(v) == 0);
         }();
         const int cm = cas_first && contest ? 1 : 0;
@@ -402,13 +402,13 @@ cudaError_t sample_chunk(const SamplerWork& w, const SamplingDev& sd, uint64_t s
             // round 0 in 128-thread blocks, up to 8 waves of them: fewer draws per thread and
             // block-level load balance for the CAS round trips (huge sampler 4.0 -> 3.5 ms/step,
             // profiles/r01_sampler_r0_shape_ab.jsonl; PCDM_R0_TPB / PCDM_R0_WAVES for A/B)
-            static const int r0_tpb = [] {
-                const char* v = getenv("PCDM_R0_TPB");
+            const int r0_tpb = [] {
+                const char* v = knob("PCDM_R0_TPB");
                 const int x = v ? atoi(v) : 128;
                 return (x == 64 || x == 128 || x == 256 || x == 512 || x == 1024) ? x : 128;
             }();
-            static const int r0_waves = [] {
-                const char* v = getenv("PCDM_R0_WAVES");
+            const int r0_waves = [] {
+                const char* v = knob("PCDM_R0_WAVES");
                 const int x = v ? atoi(v) : 8;
                 return x >= 1 && x <= 64 ? x : 8;
             }();

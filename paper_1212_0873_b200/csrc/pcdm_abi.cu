@@ -20,6 +20,14 @@
 
 using namespace pcdm_internal;
 
+namespace pcdm_internal {
+const char* knob(const char* name) {
+    const char* dbg = getenv("PCDM_DEBUG_KNOBS");
+    if (!dbg || atoi(dbg) == 0) return nullptr;
+    return getenv(name);
+}
+}  // namespace pcdm_internal
+
 namespace {
 
 thread_local std::string g_error = "no error";
@@ -322,10 +330,10 @@ int64_t choose_chunk(int64_t n, int64_t tau, int64_t iters) {
     // 128 MB per sampler pass: huge 5.90 -> 5.17 ms/step of sampler, large 6.87 -> 5.54
     // (profiles/r01_sampler_mb_ab.jsonl; 256 MB is no better)
     size_t budget = (size_t)128 << 20;
-    if (const char* mb = getenv("PCDM_SAMPLER_MB")) budget = (size_t)std::max(1, atoi(mb)) << 20;
+    if (const char* mb = knob("PCDM_SAMPLER_MB")) budget = (size_t)std::max(1, atoi(mb)) << 20;
     int64_t c = (int64_t)std::max<size_t>(1, budget / per);
     c = std::min<int64_t>(c, 8192);
-    if (const char* fc = getenv("PCDM_CHUNK")) c = std::max<int64_t>(1, atoll(fc));  // tests / tuning
+    if (const char* fc = knob("PCDM_CHUNK")) c = std::max<int64_t>(1, atoll(fc));  // tests / tuning
     return std::min<int64_t>(c, std::max<int64_t>(iters, 1));
 }
 
@@ -482,10 +490,10 @@ namespace {
 // below the threshold).  PCDM_HOT_ROWS=0 disables.
 pcdm_status select_hot_rows(pcdm_problem* p, const int* counts, cudaStream_t st, int64_t* launches) {
     p->nhot = 0;
-    const char* en = getenv("PCDM_HOT_ROWS");
+    const char* en = knob("PCDM_HOT_ROWS");
     if (en && atoi(en) == 0) return PCDM_OK;
     int hmax = 2048;
-    if (const char* hm = getenv("PCDM_HOT_MAX")) hmax = std::max(0, std::min(8192, atoi(hm)));
+    if (const char* hm = knob("PCDM_HOT_MAX")) hmax = std::max(0, std::min(8192, atoi(hm)));
     if (hmax == 0) return PCDM_OK;
     const int64_t mean = (p->nnz + p->m - 1) / p->m;
     const int64_t thr64 = std::max<int64_t>(64, 32 * mean);
@@ -586,7 +594,7 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         // logistic problems: every visited coordinate becomes nonzero, so the margins
         // s = A~ x are recomputed at each run start / refresh from a row-major copy (a warp
         // per row, fp64 in registers) instead of nnz fp64 atomics (PCDM_ROW_RESIDUAL=0: off)
-        const char* rr = getenv("PCDM_ROW_RESIDUAL");
+        const char* rr = knob("PCDM_ROW_RESIDUAL");
         if (s == PCDM_OK && loss == 1 && !(rr && atoi(rr) == 0)) {
             if (build_csr(p->csc(), counts, &p->csr, st, p->sms, &launches) == cudaSuccess) p->has_csr = true;
             else cudaGetLastError();  // out of memory: the column scatter stays
@@ -603,10 +611,10 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         // column does not at least double the lanes of an average one; ragged otherwise
         // (PCDM_LAYOUT=uniform|ragged forces one, for tests and A/B runs)
         const int64_t avg_len = (nnz + n - 1) / n;
-        const char* lay = getenv("PCDM_LAYOUT");
+        const char* lay = knob("PCDM_LAYOUT");
         bool want_ragged = lay ? strcmp(lay, "ragged") == 0
                                : (p->max_len > 62 || packed_lanes(p->max_len) > 2 * packed_lanes(avg_len));
-        if (want_ragged && !getenv("PCDM_NO_PACK")) {
+        if (want_ragged && !knob("PCDM_NO_PACK")) {
             e = build_ragged(p->csc(), p->L, p->hot_rows, p->nhot, &p->blk_off, &p->blk_cls, &p->blocks,
                              &p->ragged_chunks, st, p->sms, &launches);
             if (e == cudaSuccess) {
@@ -616,7 +624,7 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
                 want_ragged = false;
             }
         }
-        if (!p->ragged && p->max_len <= 62 && !getenv("PCDM_NO_PACK")) {
+        if (!p->ragged && p->max_len <= 62 && !knob("PCDM_NO_PACK")) {
             const int G = packed_lanes(p->max_len);
             if (cudaMalloc((void**)&p->blocks, (size_t)n * G * 16) == cudaSuccess) {
                 p->packed_G = G;
@@ -699,11 +707,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const int64_t tau = spec.tau;
     if (iters < 0 || first_iter < 0) return fail(PCDM_EINVAL, "iters and first_iter must be >= 0");
     if (first_iter + iters > (1ll << 32)) return fail(PCDM_EINVAL, "first_iter + iters must be <= 2^32");
-    if (variant < 0 || variant > 6) return fail(PCDM_EINVAL, "unknown variant %d", variant);
+    if (variant < 0 || variant > 5) return fail(PCDM_EINVAL, "unknown variant %d", variant);
     if (variant == PCDM_VARIANT_PACKED && !p->packed_G && !p->ragged)
         return fail(PCDM_EINVAL, "PACKED variant: no packed copy of A (device memory)");
-    if ((variant == PCDM_VARIANT_BATCHED || variant == PCDM_VARIANT_CLUSTER) && !p->packed_G)
-        return fail(PCDM_EINVAL, "BATCHED / CLUSTER variants need the uniform packed layout (max column length %lld%s)",
+    if (variant == PCDM_VARIANT_BATCHED && !p->packed_G)
+        return fail(PCDM_EINVAL, "BATCHED variant needs the uniform packed layout (max column length %lld%s)",
                     (long long)p->max_len, p->ragged ? ", ragged layout" : "");
     if (!(beta_override <= 1e308)) return fail(PCDM_EINVAL, "beta_override must be finite");
     CK(cudaSetDevice(p->device), "cudaSetDevice");
@@ -742,8 +750,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // the iteration kernels: huge 4.66e9 -> 4.81e9 updates/s, large / skewed 2^12 / tiny /
     // kddb_like +1-1.5 %, medium and skewed 2^16 within -0.7 % (profiles/r01_presample_overlap_ab.txt).
     // PCDM_PRESAMPLE_DEV=0: sample in the run's stream
-    const char* pe = getenv("PCDM_PRESAMPLE");
-    const char* pdev = getenv("PCDM_PRESAMPLE_DEV");
+    const char* pe = knob("PCDM_PRESAMPLE");
+    const char* pdev = knob("PCDM_PRESAMPLE_DEV");
     const bool per_pass = pdev ? atoi(pdev) != 0 : true;
     const bool presample = (!x_dev || per_pass) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
                            !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
@@ -838,7 +846,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // overrides the size rule.
     int l2_bytes = 0;
     cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, p->device);
-    const char* bat_env = getenv("PCDM_BATCHED");
+    const char* bat_env = knob("PCDM_BATCHED");
     // ... and when an iteration samples enough columns to amortise the snapshot's
     // per-iteration barrier and filter latency, with few idle slots (its passes cost per
     // slot, active or not).  Huge (profiles/r01_batched_autorule_ab.txt): tau-nice 2^17,
@@ -848,7 +856,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     double es1 = 0.0, es2 = 0.0;
     sampling_moments(spec, p->n, &es1, &es2);
     double min_slots = 131072.0;
-    if (const char* ms = getenv("PCDM_BATCHED_MIN_SLOTS")) min_slots = atof(ms);
+    if (const char* ms = knob("PCDM_BATCHED_MIN_SLOTS")) min_slots = atof(ms);
     const bool auto_batched =
         variant == PCDM_VARIANT_AUTO &&
         (bat_env ? atoi(bat_env) != 0
@@ -857,36 +865,6 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     bool batched = packed && p->packed_G > 0 && (variant == PCDM_VARIANT_BATCHED || auto_batched);
     const bool bat_fallback = batched && variant == PCDM_VARIANT_AUTO;
     if (batched && !bat_fallback) packed = false;
-    // CLUSTER (kernels_cluster.cu): r in one cluster's distributed shared memory
-    int cl_size = 0, cl_rpc = 0, cl_cap = 0;
-    size_t cl_smem = 0;
-    if (packed && !batched && p->packed_G > 0 && (variant == PCDM_VARIANT_CLUSTER || variant == PCDM_VARIANT_AUTO)) {
-        // AUTO only with PCDM_CLUSTER=1: measured slower than the grid loop on medium
-        // (5.0 vs 3.8 us per iteration, profiles/r01_cluster_medium_ab.jsonl)
-        const char* ce = getenv("PCDM_CLUSTER");
-        const bool allow = variant == PCDM_VARIANT_CLUSTER || (ce && atoi(ce) != 0);
-        // AUTO: only when every group has at most two slots per iteration on 16 CTAs
-        const bool small_tau = variant == PCDM_VARIANT_CLUSTER || tau * p->packed_G <= 2 * 16 * 1024;
-        for (int want = 16; allow && small_tau && want >= 2 && !cl_size; want >>= 1) {
-            const int64_t rpc = ((p->m + want - 1) / want + 3) & ~(int64_t)3;  // keeps the step list 8-byte aligned
-            const int64_t groups = (int64_t)want * 1024 / p->packed_G;
-            const int64_t cap = ((tau + groups - 1) / groups) * (1024 / p->packed_G);
-            const size_t smem = cluster_smem_bytes((int)std::min<int64_t>(rpc, 1 << 28), p->nhot, (int)cap);
-            if (smem > 220 * 1024) continue;
-            const int cs = cluster_plan(p->packed_G, p->loss == 1, smem, want);
-            if (cs == want) {
-                cl_size = cs;
-                cl_rpc = (int)rpc;
-                cl_cap = (int)cap;
-                cl_smem = smem;
-            }
-        }
-        if (variant == PCDM_VARIANT_CLUSTER && !cl_size)
-            return fail(PCDM_EINVAL, "CLUSTER variant: r (m = %lld) does not fit in one cluster's shared memory",
-                        (long long)p->m);
-    }
-    const bool clustered = cl_size > 0;
-    if (clustered) packed = false;
     bool one_barrier = false;
     int list_cap = 0;
     bool hot_stage = false;
@@ -910,14 +888,14 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.threads = 512;
         // CTA-long column slices staged in shared memory by bulk copies (SURVEY 8 row X2,
         // profiles/r02_bulk_stage_ab.jsonl); PCDM_BULK_STAGE=0/1 overrides
-        const char* bs_env = getenv("PCDM_BULK_STAGE");
+        const char* bs_env = knob("PCDM_BULK_STAGE");
         bulk_stage = bs_env ? atoi(bs_env) != 0 : false;
         plan.ctas = ragged_ctas(p->sms, p->loss == 1, p->nhot, bulk_stage);
         // small tau: only about as many CTAs as the average column needs lanes
         const double gavg = (double)p->ragged_chunks / (double)p->n;
         const int64_t busy = std::max<int64_t>(1, (int64_t)ceil((double)tau * gavg / plan.threads));
         if (busy < plan.ctas) plan.ctas = (int)busy;
-        if (const char* cs = getenv("PCDM_CTAS")) {
+        if (const char* cs = knob("PCDM_CTAS")) {
             const int v = atoi(cs);
             if (v >= 1) plan.ctas = std::min(v, ragged_ctas(p->sms, p->loss == 1, p->nhot, bulk_stage));
         }
@@ -927,7 +905,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         // profiles/r01_one_barrier_huge_ab.log); two barriers if the second buffer
         // cannot be allocated or PCDM_ONE_BARRIER=0
         one_barrier = true;
-        const char* ob = getenv("PCDM_ONE_BARRIER");
+        const char* ob = knob("PCDM_ONE_BARRIER");
         if (ob) one_barrier = atoi(ob) != 0;
         if (one_barrier && !p->r2 && cudaMalloc((void**)&p->r2, sizeof(float) * p->m) != cudaSuccess) {
             cudaGetLastError();
@@ -936,7 +914,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         }
         // hot-row scatters staged in shared memory per CTA (one-barrier scheme; SURVEY 8
         // row X2, profiles/r02_hot_stage_ab.jsonl); PCDM_HOT_STAGE=0/1 overrides
-        const char* hs_env = getenv("PCDM_HOT_STAGE");
+        const char* hs_env = knob("PCDM_HOT_STAGE");
         // default: dense-step workloads (logistic: every visited coordinate steps) -- skewed,
         // logistic tau = 2^16: 498 -> 31 ms of iteration kernel per 1000 iterations; LASSO's
         // sparse steps lose (169 -> 176 ms per 1e4 iterations: the per-iteration flush costs more)
@@ -954,15 +932,15 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         // (skewed tau = 2^8: 8 CTAs, 41.5 -> 36.6 ms/step); 1024-thread CTAs when 512-thread
         // ones would need more than 16 (medium: 16 x 1024, 39.2 -> 37.7 ms/step;
         // profiles/r01_cluster_sync_ab.jsonl).  PCDM_CLUSTER_SYNC=0: off
-        const char* csy = getenv("PCDM_CLUSTER_SYNC");
+        const char* csy = knob("PCDM_CLUSTER_SYNC");
         cluster_sync = one_barrier && !(csy && atoi(csy) == 0) ? 1 : 0;
         const int64_t busy1024 = (tau * p->packed_G + 1023) / 1024;
-        if (cluster_sync && busy > 16 && busy1024 <= 16 && !getenv("PCDM_CTAS")) {
+        if (cluster_sync && busy > 16 && busy1024 <= 16 && !knob("PCDM_CTAS")) {
             plan.threads = 1024;
             plan.ctas = (int)busy1024;
             cluster_sync = 2;
         }
-        if (const char* cs = getenv("PCDM_CTAS")) {
+        if (const char* cs = knob("PCDM_CTAS")) {
             const int v = atoi(cs);
             if (v >= 1)
                 plan.ctas = std::min(v, packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, 0, hot_stage));
@@ -970,7 +948,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         // dense-step workloads (logistic: every step is nonzero): stage each CTA's steps in
         // shared memory, one atomic on the list counter per CTA instead of one per step
         // (PCDM_STAGE_LIST=0/1 overrides)
-        const char* sl = getenv("PCDM_STAGE_LIST");
+        const char* sl = knob("PCDM_STAGE_LIST");
         if (sl ? atoi(sl) != 0 : p->loss == 1) {
             const int64_t groups = (int64_t)plan.ctas * plan.threads / p->packed_G;
             const int64_t cap = ((tau + groups - 1) / groups) * (plan.threads / p->packed_G);
@@ -995,19 +973,19 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // x in the block headers (packed loop): saves the separate random x line of every
     // update; PCDM_X_IN_BLOCK=0 keeps x in the caller's array.  The start-of-run
     // header load rides on the residual pass, which reads x anyway.
-    const char* xib = getenv("PCDM_X_IN_BLOCK");
-    const bool xhdr = (packed || batched || clustered) && !(xib && atoi(xib) == 0);
+    const char* xib = knob("PCDM_X_IN_BLOCK");
+    const bool xhdr = (packed || batched) && !(xib && atoi(xib) == 0);
     // dense iterates (logistic: every visited coordinate steps) keep no dirty list: its
     // appends would all hit one counter; the header passes walk all n columns instead
     // (list count pinned at ~0 = "overflowed", appends skipped with cap 0; PCDM_XLIST_DENSE)
-    const char* xde = getenv("PCDM_XLIST_DENSE");
+    const char* xde = knob("PCDM_XLIST_DENSE");
     const bool xdense = xde ? atoi(xde) != 0 : p->loss == 1;
     XHeaders xh{};
     int64_t cap_eff = 0;
     if (xhdr) {
         if (!p->xlist) {
             int64_t cap = std::min<int64_t>(p->n, (int64_t)1 << 26);
-            if (const char* xc = getenv("PCDM_XLIST_CAP")) cap = std::max<int64_t>(1, atoll(xc));
+            if (const char* xc = knob("PCDM_XLIST_CAP")) cap = std::max<int64_t>(1, atoll(xc));
             CK(cudaMalloc((void**)&p->xlist, sizeof(int) * cap), "alloc x list");
             CK(cudaMalloc((void**)&p->xlist_count, sizeof(unsigned long long)), "alloc x list");
             CK(cudaMemsetAsync(p->xlist_count, 0, sizeof(unsigned long long), st), "memset x list");
@@ -1083,7 +1061,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
         Q.pipeline = (double)p->m * 4.0 <= 0.5 * (double)l2;
-        if (const char* pl = getenv("PCDM_PIPELINE")) Q.pipeline = atoi(pl) != 0;
+        if (const char* pl = knob("PCDM_PIPELINE")) Q.pipeline = atoi(pl) != 0;
     }
     // a grid that fits one cluster (<= 16 CTAs: small tau) synchronises with the hardware
     // cluster barrier instead of the global-memory grid barrier
@@ -1094,13 +1072,13 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;
     // tau = 65536: 548 -> 179 ms/step of iteration kernel, profiles/r01_hot_rows_ab.jsonl)
     Q.hot_cache = p->nhot > 0 && (double)tau * (double)p->hot_max_count >= 1024.0 * (double)p->n;
-    if (const char* hc = getenv("PCDM_HOT_CACHE")) Q.hot_cache = p->nhot > 0 && atoi(hc) != 0;
+    if (const char* hc = knob("PCDM_HOT_CACHE")) Q.hot_cache = p->nhot > 0 && atoi(hc) != 0;
 
     BatchedParams B{};
     int bat_ctas = 0;
     // BATCHED: iterations per snapshot (the passes' unit), at most one refresh period
     int64_t bchunk = chunk;
-    if (const char* bc = getenv("PCDM_BATCHED_CHUNK")) {
+    if (const char* bc = knob("PCDM_BATCHED_CHUNK")) {
         bchunk = std::min<int64_t>(std::max<int64_t>(1, atoll(bc)), std::max<int64_t>(iters, 1));
         if (R > 0) bchunk = std::min(bchunk, R);
     }
@@ -1169,30 +1147,6 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         plan.ctas = bat_ctas;
     }
 
-    ClusterParams CP{};
-    if (clustered) {
-        CP.blocks = p->blocks;
-        CP.tau = tau;
-        CP.beta = (float)beta_d;
-        CP.lambda = (float)p->lambda;
-        CP.r = p->r;
-        CP.m = p->m;
-        CP.rpc = cl_rpc;
-        CP.x = xd;
-        CP.xlist = xhdr ? p->xlist : nullptr;
-        CP.xlist_count = p->xlist_count;
-        CP.xlist_cap = cap_eff;
-        CP.hot_rows = p->hot_rows;
-        CP.nhot = p->nhot;
-        CP.list_cap = cl_cap;
-        CP.flags = &p->sc->flags;
-        CP.nz_total = &p->sc->nz_total;
-        CP.logistic = p->loss;
-        plan.variant = PCDM_VARIANT_CLUSTER;
-        plan.lanes = p->packed_G;
-        plan.threads = 1024;
-        plan.ctas = cl_size;
-    }
 
     if (presample && !per_pass) CK(cudaStreamWaitEvent(st, p->ev_s1, 0), "join presampler");
     // iterations per launch of the iteration kernel: max(schunk, 64) (PCDM_ITER_CHUNK for
@@ -1203,7 +1157,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     int64_t ichunk = batched ? bchunk : chunk;
     if (!batched) {
         int64_t want = 64;
-        if (const char* ic = getenv("PCDM_ITER_CHUNK")) want = std::max<int64_t>(1, atoll(ic));
+        if (const char* ic = knob("PCDM_ITER_CHUNK")) want = std::max<int64_t>(1, atoll(ic));
         ichunk = std::max(schunk, std::min(want, iters));  // long launches when samples are cheap
         if (R > 0) ichunk = std::min(ichunk, R);
         ichunk = std::max<int64_t>(ichunk, 1);
@@ -1221,7 +1175,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     int64_t w0 = 0, w1 = 0;  // sampled window [w0, w1) of run-local iterations
     // the shared-memory variant refreshes the residual inside the kernel: its launches
     // are not cut at refresh points
-    const bool kernel_refresh = !packed && !batched && !clustered && plan.variant == PCDM_VARIANT_SMEM;
+    const bool kernel_refresh = !packed && !batched && plan.variant == PCDM_VARIANT_SMEM;
     if (kernel_refresh) ichunk = std::max(ichunk, std::min<int64_t>(iters, std::max<int64_t>(schunk, 1)));
     auto iter_len = [&](int64_t done) {
         int64_t c = std::min(ichunk, iters - done);
@@ -1245,13 +1199,13 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     int64_t done = 0;
     while (done < iters) {
         if (batched && bat_fallback && nz_pending) {
-            static const bool sync_check = getenv("PCDM_BATCHED_SYNC_CHECK") != nullptr;  // tests: deterministic
+            const bool sync_check = knob("PCDM_BATCHED_SYNC_CHECK") != nullptr;  // tests: deterministic
             const cudaError_t q = sync_check ? cudaEventSynchronize(p->ev_nz) : cudaEventQuery(p->ev_nz);
             if (q == cudaSuccess) {
                 nz_pending = false;
                 const double rows_per_chunk =
                     (double)*p->nz_host / (double)std::max<int64_t>(nz_at, 1) * (double)bchunk * avg_len;
-                if (rows_per_chunk > 16384.0 || getenv("PCDM_BATCHED_FORCE_FALLBACK")) {
+                if (rows_per_chunk > 16384.0 || knob("PCDM_BATCHED_FORCE_FALLBACK")) {
                     batched = false;
                     packed = true;
                     plan = packed_plan;
@@ -1287,11 +1241,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(tm.end(T_SAMPLER, ts), "event");
         int ti;
         CK(tm.begin(&ti), "event");
-        if (clustered) {
-            CP.slots = slots_c;
-            CP.iters = c;
-            CK(launch_cluster(p->packed_G, cl_size, CP, cl_smem, st, &launches), "cluster iteration kernel");
-        } else if (batched) {
+        if (batched) {
             B.slots = slots_c;
             B.iters = c;
             B.nq = (int)((c * tau + (1ll << B.cq_log) - 1) >> B.cq_log);

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpcdm.so")
 
 PCDM_OK, PCDM_EINVAL, PCDM_ENOMEM, PCDM_ECUDA, PCDM_EDIVERGED, PCDM_ESAMPLER = range(6)
-VARIANTS = {"auto": 0, "grid": 1, "smem": 2, "block": 3, "packed": 4, "batched": 5, "cluster": 6}
+VARIANTS = {"auto": 0, "grid": 1, "smem": 2, "block": 3, "packed": 4, "batched": 5}
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EDIVERGED", 5: "ESAMPLER"}
 
 EXPORTS = ["pcdm_create", "pcdm_destroy", "pcdm_last_error", "pcdm_omega", "pcdm_beta", "pcdm_run",

@@ -4,6 +4,9 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the library's tuning / test knobs (PCDM_LAYOUT, PCDM_HOT_STAGE, ...) are read only when
+# PCDM_DEBUG_KNOBS=1 (csrc/internal.h knob()); the tests force layouts and loops with them
+os.environ["PCDM_DEBUG_KNOBS"] = "1"
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

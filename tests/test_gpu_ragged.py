@@ -91,7 +91,7 @@ def test_ragged_rejects_uniform_only_loops(gpu, zipf_cols):
     inst = zipf_cols
     prob = pcdm.Problem.from_instance(inst.to(gpu))
     x = torch.zeros(inst.n, device=gpu)
-    for variant in ("batched", "cluster"):
+    for variant in ("batched",):
         with pytest.raises(pcdm.PCDMError) as e:
             prob.run(x, 8, 1, variant=variant)
         assert e.value.status == pcdm.PCDM_EINVAL

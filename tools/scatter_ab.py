@@ -30,6 +30,7 @@ def timed(prob, n, tau, iters, reps=3):
 
 
 def main():
+    os.environ["PCDM_DEBUG_KNOBS"] = "1"  # PCDM_HOT_STAGE is a debug knob
     pcdm.load()
     inst = I.generate("skewed", seed=0, device="cuda")
     gen = torch.Generator(device="cuda").manual_seed(5)
