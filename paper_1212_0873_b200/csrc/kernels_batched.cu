@@ -96,6 +96,13 @@ __device__ __forceinline__ unsigned gmask_of() {
     }
 }
 
+// lane t's 16-byte chunk of a column block inside the step kernels, which write x_i into
+// the header (chunk 0 .z) when P.xlist: the header through L2, the immutable (row, val)
+// chunks on the non-coherent path
+__device__ __forceinline__ int4 ld_blk(const BatchedParams& P, const int4* p, int t) {
+    return (t == 0 && P.xlist) ? ld_l2_v4(p) : ld_stream_v4(p);
+}
+
 // real row of a block entry (hot rows are stored as 0x80000000 | h, kernels_packed.cu)
 __device__ __forceinline__ int real_row(int v, const int* hrow) { return v < 0 ? hrow[v & 0x7fffffff] : v; }
 
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_kernel(BatchedParams
             // every CTA: the rows of iteration it-1's steps into its filter
             for (int e = grp; e < cntp; e += kThreads / G) {
                 const int i = ld_l2_s32(lidx + e);
-                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int4 c = ld_blk(P, P.blocks + (int64_t)i * G + t, t);
                 const int len = __shfl_sync(gm, c.y, src);
                 if (t == 0) bloom_set<kColLog>(s_cf, (uint32_t)i);
                 if (t > 0 && pair0 < len) bloom_set<kBloomLog>(s_bf, (uint32_t)real_row(c.x, s_hrow));
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_kernel(BatchedParams
             for (int64_t e = gid; e < cntp; e += ngroups) {
                 const int i = ld_l2_s32(lidx + e);
                 const float d = ld_l2_f32(P.nz_delta + (it - 1) * tau + e);
-                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int4 c = ld_blk(P, P.blocks + (int64_t)i * G + t, t);
                 const int len = __shfl_sync(gm, c.y, src);
                 if (t > 0 && pair0 < len) red_add_f32(DQ + real_row(c.x, s_hrow), __int_as_float(c.y) * d);
                 if (t > 0 && pair0 + 1 < len) red_add_f32(DQ + real_row(c.z, s_hrow), __int_as_float(c.w) * d);
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_kernel(BatchedParams
                 d = __shfl_sync(gm, d, src);
                 if (d != 0.0f) {
                     if (!need) {
-                        c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                        c = ld_blk(P, P.blocks + (int64_t)i * G + t, t);
                         len = __shfl_sync(gm, c.y, src);
                     }
                     if (t > 0 && pair0 < len) red_add_f32(DQ + real_row(c.x, s_hrow), __int_as_float(c.y) * d);
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
             const int* lidx = P.nz_idx + (it - 1) * tau;
             for (int e = grp; e < cntp; e += kThreads / G) {
                 const int i = ld_l2_s32(lidx + e);
-                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int4 c = ld_blk(P, P.blocks + (int64_t)i * G + t, t);
                 const int len = __shfl_sync(gm, c.y, src);
                 if (t == 0) bloom_set<kColLog>(s_cf, (uint32_t)i);
                 if (t > 0 && pair0 < len) bloom_set<kBloomLog>(s_bf, (uint32_t)real_row(c.x, s_hrow));
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
             for (int64_t e = gid; e < cntp; e += ngroups) {
                 const int i = ld_l2_s32(lidx + e);
                 const float d = ld_l2_f32(P.nz_delta + (it - 1) * tau + e);
-                const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+                const int4 c = ld_blk(P, P.blocks + (int64_t)i * G + t, t);
                 const int len = __shfl_sync(gm, c.y, src);
                 if (t > 0 && pair0 < len) red_add_f32(DQ + real_row(c.x, s_hrow), __int_as_float(c.y) * d);
                 if (t > 0 && pair0 + 1 < len) red_add_f32(DQ + real_row(c.z, s_hrow), __int_as_float(c.w) * d);
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 2) pcdm_batched_slot_kernel(BatchedP
             const int pos = atomicAdd(P.nz_count + it, 1);
             P.nz_idx[it * tau + pos] = i;
             P.nz_delta[it * tau + pos] = d;
-            if (len < 0) len = ld_stream_v4(blk).y;
+            if (len < 0) len = (P.xlist ? ld_l2_v4(blk) : ld_stream_v4(blk)).y;
 #pragma unroll
             for (int l = 1; l < G; ++l) {
                 if (2 * (l - 1) >= len) break;

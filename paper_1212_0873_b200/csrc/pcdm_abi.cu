@@ -1076,12 +1076,13 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
 
     BatchedParams B{};
     int bat_ctas = 0;
-    // BATCHED: iterations per snapshot (the passes' unit), at most one refresh period
-    int64_t bchunk = chunk;
-    if (const char* bc = knob("PCDM_BATCHED_CHUNK")) {
-        bchunk = std::min<int64_t>(std::max<int64_t>(1, atoll(bc)), std::max<int64_t>(iters, 1));
-        if (R > 0) bchunk = std::min(bchunk, R);
-    }
+    // BATCHED: iterations per snapshot (the passes' unit), its own rule independent of the
+    // sampler pass size: 18 (huge: the best of 9..36 with the sampler pass held fixed,
+    // profiles/r01_batched_chunk_ab.txt), at most one refresh period and the run
+    int64_t bchunk = 18;
+    if (const char* bc = knob("PCDM_BATCHED_CHUNK")) bchunk = std::max<int64_t>(1, atoll(bc));
+    bchunk = std::min<int64_t>(bchunk, std::max<int64_t>(iters, 1));
+    if (R > 0) bchunk = std::min(bchunk, R);
     if (batched) {
         const int64_t chunk = bchunk;
         const int G = p->packed_G;
@@ -1374,6 +1375,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     stats.iter_kernel_ms = tms[T_ITER];
     stats.sampler_ms = tms[T_SAMPLER];
     if (presample) {
+        // the run's stream waited only for the pass events: ev_s1 may still be pending
+        cudaEventSynchronize(p->ev_s1);
         float pms = 0.f;
         if (cudaEventElapsedTime(&pms, p->ev_s0, p->ev_s1) == cudaSuccess) stats.sampler_ms += pms;
         cudaGetLastError();
