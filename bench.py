@@ -583,6 +583,8 @@ def bench_ours(args, world, rank, local):
         "async": bool(args.async_),
         "F_final": F_final, "nonzero_step_frac": nz / (K * size * iters),
         "variant": VARIANT_NAMES.get(st0["variant"], "?"),
+        "screen_per_step": {f: sum(s.get("screen_" + f, 0) for s in st_list) / K
+                            for f in ("misses", "scans", "spec", "flagged")},
         "grid": {"ctas": st0["grid_ctas"], "threads": st0["threads_per_cta"], "lanes_per_column": st0["lanes_per_column"]},
         "setup_s": {"generate": gen_s, "create": create_s},
         "parity": par,

@@ -140,6 +140,12 @@ typedef struct {
     int64_t host_d2h_bytes;     /* host x: bytes copied device -> host (the changed
                                    entries only, as (index, value) pairs, when they are
                                    fewer than n/2; else the whole x)                  */
+    int64_t screen_misses;      /* BATCHED, screened step pass: iterations in which a
+                                   flagged (not speculative) slot took a nonzero step  */
+    int64_t screen_scans;       /* ... and the later-slot scans those steps cost        */
+    int64_t screen_spec;        /* ... speculative items (nonzero step from g0 alone)    */
+    int64_t screen_flagged;     /* ... flagged items (share a row or the column with an
+                                   earlier speculative step of the chunk)               */
 } pcdm_run_stats;
 
 /* pcdm_create -- build a problem handle for LASSO with A (m x n, CSC), b, lambda.

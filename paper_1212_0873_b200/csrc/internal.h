@@ -250,6 +250,20 @@ struct BatchedParams {
     const int* hot_rows;
     int nhot;
     int logistic;
+    // SCREENED step pass (LASSO; kernels_batched.cu passes 3s-4s): no grid barrier per
+    // iteration.  The sweep takes every slot's step from g0 alone (the "speculative" step),
+    // the test pass flags the slots a speculative step of an earlier iteration of the
+    // chunk could change (shared row or column), and one CTA replays the chunk's
+    // iterations over the speculative and flagged slots only, with the exact corrections.
+    int screen;           // 1: passes 3s-4s replace pass 3 + fold
+    int2* lx;             // [iters * tau] {L_i, x_i at the chunk start} (pass 1; L = -1 bits: idle slot)
+    int* rows;            // [nrow][rows_ld] real rows of every slot (pass 1; -1: none)
+    int64_t rows_ld;      // leading dimension of rows (>= iters * tau)
+    int nrow;             // rows stored per slot (max column length)
+    unsigned* bits;       // [ceil(rows_ld / 32)] slot is already an item (zero between chunks)
+    int* items;           // [2][rows_ld]: speculative slots, then flagged slots
+    int* counts;          // [4]: #speculative, #flagged, misses (run total), scans (run total)
+    int fix_cap;          // debug: cap on the fix-up's staged items / map sizes (0 = by shared memory)
 };
 size_t batched_step_smem(int nhot);
 int batched_cq_log(int G);

@@ -62,6 +62,9 @@ constexpr int kSweepMaxSlots = 40 * 512;  // pass 2: slots per CTA (x 4 B of sha
 #ifndef PCDM_BATCHED_UP
 #define PCDM_BATCHED_UP 1  // pass 3: slots per thread loaded before the filter update
 #endif
+#ifndef PCDM_EXPAND_PREFETCH
+#define PCDM_EXPAND_PREFETCH 0  // pass 1: the next range's first slots loaded ahead (spills at 64 registers)
+#endif
 #ifndef PCDM_EXPAND_MINB
 #define PCDM_EXPAND_MINB 2
 #endif
@@ -145,23 +148,38 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
     const int64_t total = P.iters * P.tau;
     const int rmask = (1 << P.rb) - 1;
 
+    // U slots per group in flight: the slot ids, then their blocks, then the entries;
+    // the first U of the next range are loaded before this range's sort and write phases
+    constexpr int U = PCDM_EXPAND_U;
+    constexpr int GPC = kExpandThreads / G;  // groups per CTA
+    auto load_round = [&](int q, int sl0, int (&iv)[U], int4 (&cv)[U]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t tt = ((int64_t)q << P.cq_log) + sl0 + u * GPC;
+            iv[u] = (sl0 + u * GPC < cq && tt < total) ? ld_stream_s32(P.slots + tt) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (iv[u] >= 0) cv[u] = ld_stream_v4(P.blocks + (int64_t)iv[u] * G + t);
+    };
+    int ivn[U];
+    int4 cvn[U];
+    if (PCDM_EXPAND_PREFETCH && (int)blockIdx.x < P.nq) load_round(blockIdx.x, grp, ivn, cvn);
     for (int q = blockIdx.x; q < P.nq; q += gridDim.x) {
         for (int b = threadIdx.x; b < P.nb; b += blockDim.x) cnt[b] = 0;
         __syncthreads();
-        // U slots per group in flight: the slot ids, then their blocks, then the entries
-        constexpr int U = PCDM_EXPAND_U;
-        constexpr int GPC = kExpandThreads / G;  // groups per CTA
         for (int sl0 = grp; sl0 < cq; sl0 += GPC * U) {
             int iv[U];
             int4 cv[U];
+            if (PCDM_EXPAND_PREFETCH && sl0 == grp) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t tt = ((int64_t)q << P.cq_log) + sl0 + u * GPC;
-                iv[u] = (sl0 + u * GPC < cq && tt < total) ? ld_stream_s32(P.slots + tt) : -1;
+                for (int u = 0; u < U; ++u) {
+                    iv[u] = ivn[u];
+                    cv[u] = cvn[u];
+                }
+            } else {
+                load_round(q, sl0, iv, cv);
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (iv[u] >= 0) cv[u] = ld_stream_v4(P.blocks + (int64_t)iv[u] * G + t);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int sl = sl0 + u * GPC;
@@ -188,12 +206,27 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
                     stage[e0] = ea;
                     stage[e0 + 1] = eb;
                 }
-                // the slot record of pass 3, 8 bytes per lane: lane 0 {L_i, x_i}, lane t the
-                // real rows of its two entries (-1 = none)
-                if (tt < total && t < 2 * P.rnv)
+                if (tt < total && P.screen) {
+                    // screened step pass: {L_i, x_i} per slot (L = -1 bits: idle slot) and the
+                    // slot's real rows, row-major by entry (coalesced for the test pass)
+                    if (t == 0) {
+                        int2 lx = make_int2(-1, 0);
+                        if (iv[u] >= 0)
+                            lx = make_int2(cv[u].x, P.xlist ? cv[u].z : __float_as_int(ld_l2_f32(P.x + iv[u])));
+                        P.lx[tt] = lx;
+                    } else {
+                        const int p0 = 2 * (t - 1);
+                        if (p0 < P.nrow) P.rows[p0 * P.rows_ld + tt] = ea.x;
+                        if (p0 + 1 < P.nrow) P.rows[(p0 + 1) * P.rows_ld + tt] = eb.x;
+                    }
+                } else if (tt < total && t < 2 * P.rnv) {
+                    // the slot record of pass 3, 8 bytes per lane: lane 0 {L_i, x_i}, lane t the
+                    // real rows of its two entries (-1 = none)
                     P.rec[tt * 2 * P.rnv + t] = t == 0 ? make_int2(cv[u].x, cv[u].z) : make_int2(ea.x, eb.x);
+                }
             }
         }
+        if (PCDM_EXPAND_PREFETCH && q + (int)gridDim.x < P.nq) load_round(q + gridDim.x, grp, ivn, cvn);
         __syncthreads();
         if (threadIdx.x < 32) {  // exclusive scan of the bin counts (one warp, 32 bins per step)
             int carry = 0;
@@ -262,37 +295,86 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
             lo = __ldg(offs);
             hi = __ldg(offs + 1);
         };
-        int lo = 0, hi = 0;
-        if (hw < nseg) bounds(hw, lo, hi);
+        // the first HW * U entries of the next segment are loaded before the current
+        // segment's gathers (software pipelining: one segment's entries always in flight)
+        constexpr int U = 6;
+        auto first_chunk = [&](int sg, int lo, int hi, int2 (&e)[U]) {
+            const int bb = sg / nql, ql = sg - bb * nql;
+            const int2* ent = P.gent + (int64_t)(q0 + ql) * ne;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (lo + hl + HW * u < hi) e[u] = ld_stream_v2(ent + lo + hl + HW * u);
+        };
+        int lo = 0, hi = 0, nlo = 0, nhi = 0;
+        int2 ec[U];
+        if (hw < nseg) {
+            bounds(hw, lo, hi);
+            first_chunk(hw, lo, hi, ec);
+        }
+        if (hw + NH < nseg) bounds(hw + NH, nlo, nhi);
         for (int sg = hw; sg < nseg; sg += NH) {
-            int nlo = 0, nhi = 0;
-            if (sg + NH < nseg) bounds(sg + NH, nlo, nhi);
+            int2 en[U];
+            if (sg + NH < nseg) first_chunk(sg + NH, nlo, nhi, en);
+            int n2lo = 0, n2hi = 0;
+            if (sg + 2 * NH < nseg) bounds(sg + 2 * NH, n2lo, n2hi);
             const int bb = sg / nql, ql = sg - bb * nql;
             const int2* ent = P.gent + (int64_t)(q0 + ql) * ne;
             const float* rb = P.r + ((int64_t)bb << P.rb);
             float* acc = s_g + (ql << P.cq_log);
-            constexpr int U = 8;
-            for (int x0 = lo + hl; x0 < hi; x0 += HW * U) {
-                int2 e[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (x0 + HW * u < hi) e[u] = ld_stream_v2(ent + x0 + HW * u);
+            {
                 float rv[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (x0 + HW * u < hi) rv[u] = __ldcg(rb + (e[u].x & rmask));
+                    if (lo + hl + HW * u < hi) rv[u] = __ldcg(rb + (ec[u].x & rmask));
 #pragma unroll
                 for (int u = 0; u < U; ++u)
+                    if (lo + hl + HW * u < hi)
+                        atomicAdd(acc + ((unsigned)ec[u].x >> P.rb), __int_as_float(ec[u].y) * grad_weight<LOGISTIC>(rv[u]));
+            }
+            constexpr int U2 = 4;  // the rest of a long segment (few registers: en is live)
+            for (int x0 = lo + hl + HW * U; x0 < hi; x0 += HW * U2) {
+                int2 e[U2];
+#pragma unroll
+                for (int u = 0; u < U2; ++u)
+                    if (x0 + HW * u < hi) e[u] = ld_stream_v2(ent + x0 + HW * u);
+                float rv[U2];
+#pragma unroll
+                for (int u = 0; u < U2; ++u)
+                    if (x0 + HW * u < hi) rv[u] = __ldcg(rb + (e[u].x & rmask));
+#pragma unroll
+                for (int u = 0; u < U2; ++u)
                     if (x0 + HW * u < hi)
                         atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u) ec[u] = en[u];
             lo = nlo;
             hi = nhi;
+            nlo = n2lo;
+            nhi = n2hi;
         }
         __syncthreads();
         float* g0 = P.g0 + ((int64_t)q0 << P.cq_log);
         const int64_t left = total - ((int64_t)q0 << P.cq_log);
-        for (int k = threadIdx.x; k < nacc && k < left; k += blockDim.x) g0[k] = s_g[k];
+        for (int k = threadIdx.x; k < nacc && k < left; k += blockDim.x) {
+            const float g = s_g[k];
+            g0[k] = g;
+            if (!LOGISTIC && P.screen) {
+                // the speculative step: the slot's step if no earlier step of the chunk
+                // touched its rows or its column (the fix-up's arithmetic in that case, bit
+                // for bit); nonzero ones become items of the fix-up
+                const int64_t t = ((int64_t)q0 << P.cq_log) + k;
+                const int2 lx = ld_stream_v2(P.lx + t);
+                if (lx.x != -1) {
+                    const float xi = __int_as_float(lx.y);
+                    const float xp = prox_l1(xi, g, P.beta * __int_as_float(lx.x), P.lambda);
+                    if (xp - xi != 0.0f) {
+                        atomicOr(P.bits + (t >> 5), 1u << (t & 31));
+                        P.items[atomicAdd(P.counts, 1)] = (int)t;
+                    }
+                }
+            }
+        }
         __syncthreads();
     }
 }
@@ -613,6 +695,523 @@ __global__ void batch_fold_kernel(BatchedParams P) {
     if (nz) atomicAdd(P.nz_total, nz);
 }
 
+// ---------------------------------------------------------------- screened step pass
+// Pass 3 without a grid barrier per iteration (LASSO).  The sweep's epilogue took every
+// slot's step from g0 alone, the step the slot takes exactly when no earlier step of the
+// chunk changed a row of its column or its x_i; the nonzero ones are the speculative
+// items.  Synchronous PCDM1 (alg:PCD1) differs from that only at
+// slots sharing a row or the column with a step of an earlier iteration of the chunk:
+//   3s test:  every slot of iteration k is tested against the rows and columns of the
+//             speculative steps of iterations < k (a shared-memory key table with the
+//             earliest iteration per key); hits become flagged items;
+//   4s fix:   one CTA replays the chunk's iterations over the items only, in order: g =
+//             g0 + sum of val * D[row] over the rows the chunk's earlier true steps
+//             dirtied (D in a shared-memory map), x_i current if the column stepped earlier;
+//             a nonzero step updates x_i, D and r (the fold) at once.  A flagged item that
+//             steps is a "miss": its rows were not tested against, so the CTA scans the
+//             later slots for them before going on.
+// Same arithmetic as pass 3 per slot (g0 + corrections in fp32); items that never touch a
+// dirty row take exactly the speculative step.
+constexpr int kTestThreads = 1024;
+constexpr int kTestLog = 14;  // test key table: 2^14 {key, iteration} pairs = 128 KB
+constexpr int kColKey = (int)0x80000000;  // column keys i | 2^31 (rows are >= 0)
+
+__device__ __forceinline__ uint32_t key_hash(uint32_t v, int log) { return (v * 0x9E3779B1u) >> (32 - log); }
+
+// keep the minimum stamp per key (open addressing, linear probing; never full: the
+// callers keep the load <= 1/2)
+__device__ __forceinline__ void stamp_insert(int* keys, int* stamps, int log, int key, int stamp) {
+    const uint32_t mask = (1u << log) - 1u;
+    uint32_t h = key_hash((uint32_t)key, log);
+    for (;;) {
+        const int prev = atomicCAS(keys + h, -1, key);
+        if (prev == -1 || prev == key) {
+            atomicMin(stamps + h, stamp);
+            return;
+        }
+        h = (h + 1) & mask;
+    }
+}
+__device__ __forceinline__ int stamp_find(const int* keys, const int* stamps, int log, int key) {
+    const uint32_t mask = (1u << log) - 1u;
+    uint32_t h = key_hash((uint32_t)key, log);
+    for (;;) {
+        const int k = keys[h];
+        if (k == key) return stamps[h];
+        if (k == -1) return 0x7fffffff;
+        h = (h + 1) & mask;
+    }
+}
+
+// slot t of the chunk becomes an item (once)
+__device__ __forceinline__ bool claim_slot(unsigned* bits, int64_t t) {
+    const unsigned bit = 1u << (t & 31);
+    return !(atomicOr(bits + (t >> 5), bit) & bit);
+}
+
+// test pass over slots [t0, t1) against the keys in the table: a thread takes 4
+// consecutive slots (16-byte row loads; rows_ld is a multiple of 4), all their rows in
+// flight before the probes
+__device__ __forceinline__ void test_slots(const BatchedParams& P, const int* keys, const int* stamps, int log,
+                                           int64_t t0, int64_t t1, int64_t tid, int64_t nth, int* out,
+                                           int* out_count) {
+    const int64_t tau = P.tau;
+    constexpr int PB = 6;  // rows per batch of loads
+    for (int64_t tb = (t0 & ~(int64_t)3) + 4 * tid; tb < t1; tb += 4 * nth) {
+        int iv[4];
+        bool hit[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            iv[u] = tb + u >= t0 && tb + u < t1 ? ld_stream_s32(P.slots + tb + u) : -1;
+            hit[u] = false;
+        }
+        const int kb = (int)(tb / tau);
+        int ks[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ks[u] = (int)((tb + u) / tau);
+        (void)kb;
+        for (int p0 = 0; p0 < P.nrow; p0 += PB) {
+            int4 rv[PB];
+#pragma unroll
+            for (int u = 0; u < PB; ++u)
+                rv[u] = p0 + u < P.nrow ? ld_stream_v4((const int4*)(P.rows + (int64_t)(p0 + u) * P.rows_ld + tb))
+                                        : make_int4(-1, -1, -1, -1);
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                hit[0] |= rv[u].x >= 0 && stamp_find(keys, stamps, log, rv[u].x) < ks[0];
+                hit[1] |= rv[u].y >= 0 && stamp_find(keys, stamps, log, rv[u].y) < ks[1];
+                hit[2] |= rv[u].z >= 0 && stamp_find(keys, stamps, log, rv[u].z) < ks[2];
+                hit[3] |= rv[u].w >= 0 && stamp_find(keys, stamps, log, rv[u].w) < ks[3];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (iv[u] < 0) continue;
+            const bool h = hit[u] || stamp_find(keys, stamps, log, iv[u] | kColKey) < ks[u];
+            if (h && claim_slot(P.bits, tb + u)) out[atomicAdd(out_count, 1)] = (int)(tb + u);
+        }
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kTestThreads, 1) screen_test_kernel(BatchedParams P) {
+    extern __shared__ int s_kt[];
+    int* keys = s_kt;
+    int* stamps = s_kt + (1 << kTestLog);
+    __shared__ int s_kmin;
+    const int t = threadIdx.x & (G - 1);
+    const unsigned gm = gmask_of<G>();
+    const int src = (threadIdx.x & 31) & ~(G - 1);
+    const int pair0 = 2 * (t - 1);
+    const int64_t tau = P.tau;
+    const int64_t total = P.iters * tau;
+    const int nspec = ld_l2_s32(P.counts);
+    // speculative slots per table fill (keys <= half the table)
+    const int per = std::max(1, ((1 << kTestLog) / 2) / (1 + P.nrow));
+    for (int b0 = 0; b0 < nspec; b0 += per) {
+        for (int w = threadIdx.x; w < (1 << kTestLog); w += blockDim.x) {
+            keys[w] = -1;
+            stamps[w] = 0x7fffffff;
+        }
+        if (threadIdx.x == 0) s_kmin = 0x7fffffff;
+        __syncthreads();
+        const int b1 = std::min(nspec, b0 + per);
+        // one group of G lanes per speculative slot: its column and its rows, stamped with
+        // the slot's iteration
+        for (int q = b0 + (int)(threadIdx.x / G); q < b1; q += blockDim.x / G) {
+            const int ts = ld_l2_s32(P.items + q);
+            const int k = (int)(ts / tau);
+            const int i = ld_stream_s32(P.slots + ts);
+            const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+            const int len = __shfl_sync(gm, c.y, src);
+            if (t == 0) {
+                stamp_insert(keys, stamps, kTestLog, i | kColKey, k);
+                atomicMin(&s_kmin, k);
+            } else {
+                if (pair0 < len) stamp_insert(keys, stamps, kTestLog, real_row(c.x, P.hot_rows), k);
+                if (pair0 + 1 < len) stamp_insert(keys, stamps, kTestLog, real_row(c.z, P.hot_rows), k);
+            }
+        }
+        __syncthreads();
+        // slots of iterations after the earliest stamp
+        const int64_t t0 = ((int64_t)s_kmin + 1) * tau;
+        test_slots(P, keys, stamps, kTestLog, t0, total, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                   (int64_t)gridDim.x * blockDim.x, P.items + P.rows_ld, P.counts + 1);
+        __syncthreads();
+    }
+}
+
+// fix-up shared-memory shape (host-computed from the shared-memory budget)
+struct FixShape {
+    int icap;  // items staged in shared memory (meta + nl block lanes each)
+    int nl;    // 16-byte lanes staged per item (1 + ceil(max length / 2))
+    int dlog;  // D map: 2^dlog {row, value} entries
+    int clog;  // stepped-column set: 2^clog keys
+    int scap;  // steps of one iteration kept in shared memory (the rest in the global list)
+    int mlog;  // miss-scan key table: 2^mlog {key, stamp}
+    int c;     // iterations of the chunk (histogram size)
+};
+
+size_t fix_smem_bytes(const FixShape& F) {
+    return (size_t)F.icap * 16 * (1 + F.nl) + ((size_t)8 << F.dlog) + ((size_t)4 << F.clog) + (size_t)F.icap * 4 +
+           (size_t)F.scap * 8 + ((size_t)8 << F.mlog) + (size_t)(F.c + 1) * 8;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kTestThreads, 1) screen_fix_kernel(BatchedParams P, FixShape F) {
+    extern __shared__ int4 s_fix[];
+    int4* s_meta = s_fix;                        // [icap] {t, i, g0, x0}
+    int4* s_blk = s_meta + F.icap;               // [icap][nl] the item's block
+    int* s_dkey = (int*)(s_blk + (size_t)F.icap * F.nl);
+    float* s_dval = (float*)(s_dkey + (1 << F.dlog));
+    int2* s_step = (int2*)(s_dval + (1 << F.dlog));  // [scap] {item, delta}
+    int* s_ckey = (int*)(s_step + F.scap);
+    int* s_ord = s_ckey + (1 << F.clog);         // [icap] items by iteration
+    int* s_mkey = s_ord + F.icap;                // [2^mlog] miss keys
+    int* s_mstamp = s_mkey + (1 << F.mlog);
+    int* s_start = s_mstamp + (1 << F.mlog);     // [c + 1]
+    int* s_cur = s_start + (F.c + 1);            // [c]
+    __shared__ int s_nstep, s_dcount, s_ccount, s_dspill, s_cfull, s_miss, s_nextra, s_mcount, s_total, s_nmiss,
+        s_nscan;
+
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
+    const int64_t tau = P.tau;
+    const int c = (int)P.iters;
+    const int nspec = ld_l2_s32(P.counts), ncand = ld_l2_s32(P.counts + 1);
+    const int nit = nspec + ncand;
+    // items q < nstaged live in shared memory (at most two per thread; scan hits: q >= nit)
+    const int nstaged = min(nit, min(F.icap, 2 * nth));
+    int* const cand = P.items + P.rows_ld;       // flagged items, then the misses' scans
+    int* const ord = nit <= F.icap ? s_ord : P.items + 2 * P.rows_ld;
+    auto item_t = [&](int q) { return q < nspec ? ld_l2_s32(P.items + q) : ld_l2_s32(cand + (q - nspec)); };
+    const int dmask = (1 << F.dlog) - 1, cmask = (1 << F.clog) - 1;
+    const int dlimit = (7 << F.dlog) / 10, climit = (7 << F.clog) / 10;
+
+    long long tclk0 = clock64();
+    for (int w = tid; w < (1 << F.dlog); w += nth) {
+        s_dkey[w] = -1;
+        s_dval[w] = 0.0f;
+    }
+    for (int w = tid; w < (1 << F.clog); w += nth) s_ckey[w] = -1;
+    for (int w = tid; w <= c; w += nth) s_start[w] = 0;
+    if (tid == 0) {
+        s_nstep = s_dcount = s_ccount = s_dspill = s_cfull = s_miss = s_nextra = s_total = s_nmiss = s_nscan = 0;
+    }
+    __syncthreads();
+    // stage the items (slot id, g0, x0 and the column's block); count them per iteration
+    // with warp-aggregated atomics (one per distinct iteration in a warp), each item
+    // keeping its rank within its iteration
+    int my_k[2], my_rank[2];  // this thread's items q = tid and tid + nth (nit <= 2 nth here)
+    for (int r = 0, q = tid; r < 2; ++r, q += nth) {
+        my_k[r] = -1;
+        const bool has = q < nit;
+        int t = 0, k = -1;
+        if (has) {
+            t = item_t(q);
+            k = (int)(t / tau);
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, has);
+        if (has) {
+            const unsigned peers = __match_any_sync(act, k);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(s_start + k, __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            my_k[r] = k;
+            my_rank[r] = base + __popc(peers & ((1u << lane) - 1u));
+        }
+        if (has && q < nstaged) {
+            const int i = ld_stream_s32(P.slots + t);
+            const int4* blk = P.blocks + (int64_t)i * G;
+            int4 bl[8];
+#pragma unroll
+            for (int l = 0; l < 8; ++l)
+                if (l < F.nl) bl[l] = ld_stream_v4(blk + l);
+            const float g0 = ld_l2_f32(P.g0 + t);
+#pragma unroll
+            for (int l = 0; l < 8; ++l)
+                if (l < F.nl) s_blk[(size_t)q * F.nl + l] = bl[l];
+            for (int l = 8; l < F.nl; ++l) s_blk[(size_t)q * F.nl + l] = ld_stream_v4(blk + l);
+            const float x0 = P.xlist ? __int_as_float(bl[0].z) : ld_l2_f32(P.x + i);
+            s_meta[q] = make_int4(t, i, __float_as_int(g0), __float_as_int(x0));
+        }
+    }
+    __syncthreads();  // the ranks above count ranked items only
+    for (int q = 2 * nth + tid; q < nit; q += nth) {  // beyond 2 per thread: not staged, plain atomics
+        const int t = item_t(q);
+        atomicAdd(s_start + t / tau, 1);
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the per-iteration counts, 32 iterations per step
+        int carry = 0;
+        for (int k0 = 0; k0 < c; k0 += 32) {
+            const int k = k0 + tid;
+            const int v = k < c ? s_start[k] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            if (k < c) {
+                s_start[k] = carry + incl - v;
+                s_cur[k] = carry + incl;  // items beyond 2 per thread are appended after the ranked ones
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (tid == 0) s_start[c] = carry;
+    }
+    __syncthreads();
+    // ranked items go to start + rank; the rest (nit > 2 nth) are placed from the end of
+    // their iteration's range backwards
+    for (int r = 0; r < 2; ++r)
+        if (my_k[r] >= 0) ord[s_start[my_k[r]] + my_rank[r]] = tid + r * nth;
+    for (int q = 2 * nth + tid; q < nit; q += nth) ord[atomicSub(s_cur + item_t(q) / tau, 1) - 1] = q;
+    __syncthreads();
+
+    // (every probe loop is bounded by the table size: concurrent inserts may overshoot the
+    // load limit and fill a small table)
+    auto dget = [&](int row) -> float {
+        float v = 0.0f;
+        int h = (int)key_hash((uint32_t)row, F.dlog);
+        for (int pr = 0; pr <= dmask; ++pr) {
+            const int k = s_dkey[h];
+            if (k == row) {
+                v = s_dval[h];
+                break;
+            }
+            if (k == -1) break;
+            h = (h + 1) & dmask;
+        }
+        if (s_dspill) v += ld_l2_f32(P.d0 + row);
+        return v;
+    };
+    auto dadd = [&](int row, float v) {
+        int h = (int)key_hash((uint32_t)row, F.dlog);
+        for (int pr = 0; pr <= dmask; ++pr) {
+            const int k = ((volatile int*)s_dkey)[h];
+            if (k == row) {
+                atomicAdd(s_dval + h, v);
+                return;
+            }
+            if (k == -1) {
+                if (*(volatile int*)&s_dcount >= dlimit) break;
+                const int prev = atomicCAS(s_dkey + h, -1, row);
+                if (prev == -1) atomicAdd(&s_dcount, 1);
+                if (prev == -1 || prev == row) {
+                    atomicAdd(s_dval + h, v);
+                    return;
+                }
+            }
+            h = (h + 1) & dmask;
+        }
+        s_dspill = 1;  // map full: this row's deltas go to the dense global buffer
+        red_add_f32(P.d0 + row, v);
+    };
+    auto stepped = [&](int i) -> bool {  // column stepped earlier in the chunk (conservative)
+        if (s_cfull) return true;
+        int h = (int)key_hash((uint32_t)i, F.clog);
+        for (int pr = 0; pr <= cmask; ++pr) {
+            const int k = s_ckey[h];
+            if (k == i) return true;
+            if (k == -1) return false;
+            h = (h + 1) & cmask;
+        }
+        return true;  // table full without the key: conservative
+    };
+    auto mark_stepped = [&](int i) {
+        int h = (int)key_hash((uint32_t)i, F.clog);
+        for (int pr = 0; pr <= cmask; ++pr) {
+            const int k = ((volatile int*)s_ckey)[h];
+            if (k == i) return;
+            if (k == -1) {
+                if (*(volatile int*)&s_ccount >= climit) break;
+                const int prev = atomicCAS(s_ckey + h, -1, i);
+                if (prev == -1) atomicAdd(&s_ccount, 1);
+                if (prev == -1 || prev == i) return;
+            }
+            h = (h + 1) & cmask;
+        }
+        s_cfull = 1;
+    };
+    auto cur_x = [&](int i) -> float {
+        return P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : ld_l2_f32(P.x + i);
+    };
+    // entry e of a block given as lanes (staged copy or global)
+    auto entry = [&](const int4* lanes, int e, bool staged) -> int2 {
+        const int4 v = staged ? lanes[1 + (e >> 1)] : ld_stream_v4(lanes + 1 + (e >> 1));
+        return (e & 1) ? make_int2(v.z, v.w) : make_int2(v.x, v.y);
+    };
+    // compute phase of one item of iteration k, one warp per item: lane e takes entry e
+    // (and e + 32, ...), the corrections are summed over the warp (a thread walking the
+    // entries serialised the lanes' divergent map probes: ~12 K cycles per iteration)
+    auto process = [&](int q, int k) {
+        const bool staged = q < nstaged;
+        int i;
+        float g0, x0;
+        const int4* lanes;
+        int4 h;
+        if (staged) {
+            const int4 m = s_meta[q];
+            i = m.y;
+            g0 = __int_as_float(m.z);
+            x0 = __int_as_float(m.w);
+            lanes = s_blk + (size_t)q * F.nl;
+            h = lanes[0];
+        } else {
+            const int t = item_t(q);
+            i = ld_stream_s32(P.slots + t);
+            g0 = ld_l2_f32(P.g0 + t);
+            lanes = P.blocks + (int64_t)i * G;
+            h = ld_l2_v4(lanes);
+            x0 = P.xlist ? __int_as_float(h.z) : ld_l2_f32(P.x + i);  // current x_i (this kernel writes it)
+        }
+        const int len = h.y;
+        float corr = 0.0f;
+        for (int e = lane; e < len; e += 32) {
+            const int2 rv = entry(lanes, e, staged);
+            const float dv = dget(real_row(rv.x, P.hot_rows));
+            if (dv != 0.0f) corr += __int_as_float(rv.y) * dv;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) corr += __shfl_xor_sync(0xffffffffu, corr, o);
+        if (lane != 0) return;
+        const float xi = staged && stepped(i) ? cur_x(i) : x0;
+        const float xp = prox_l1(xi, g0 + corr, P.beta * __int_as_float(h.x), P.lambda);
+        const float d = xp - xi;
+        if (d == 0.0f) return;
+        if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
+        if (P.xlist) ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
+        else P.x[i] = xp;
+        const int pos = atomicAdd(&s_nstep, 1);
+        if (pos < F.scap) s_step[pos] = make_int2(q, __float_as_int(d));
+        P.nz_idx[k * tau + pos] = i;
+        P.nz_delta[k * tau + pos] = d;
+        if (q >= nspec) s_miss = 1;
+    };
+    // apply phase, one warp per step e of iteration k: D, r (the fold) and the
+    // stepped-column set
+    auto apply = [&](int e, int k) {
+        int q = -1, i;
+        float d;
+        if (e < F.scap) {
+            const int2 st = s_step[e];
+            q = st.x;
+            d = __int_as_float(st.y);
+            i = q < nstaged ? s_meta[q].y : ld_l2_s32(P.nz_idx + k * tau + e);
+        } else {
+            i = ld_l2_s32(P.nz_idx + k * tau + e);
+            d = ld_l2_f32(P.nz_delta + k * tau + e);
+        }
+        const bool staged = q >= 0 && q < nstaged;
+        const int4* lanes = staged ? s_blk + (size_t)q * F.nl : P.blocks + (int64_t)i * G;
+        const int len = staged ? lanes[0].y : ld_l2_v4(lanes).y;
+        for (int ee = lane; ee < len; ee += 32) {
+            const int2 rv = entry(lanes, ee, staged);
+            const int row = real_row(rv.x, P.hot_rows);
+            const float v = __int_as_float(rv.y) * d;
+            dadd(row, v);
+            red_add_f32(P.r_out + row, v);
+        }
+        if (lane == 0) {
+            mark_stepped(i);
+            if (P.xlist && P.xlist_cap > 0) {
+                const unsigned long long qq = atomicAdd(P.xlist_count, 1ull);
+                if (qq < (unsigned long long)P.xlist_cap) P.xlist[qq] = i;
+            }
+        }
+    };
+
+    const int64_t total = P.iters * tau;
+    long long tclk1 = clock64(), tcomp = 0, tapply = 0;
+    for (int k = 0; k < c; ++k) {
+        long long ta = clock64();
+        for (int p = s_start[k] + warp; p < s_start[k + 1]; p += nwarp) process(ord[p], k);
+        // items added by the scans for earlier misses
+        const int nextra = s_nextra;
+        for (int e = warp; e < nextra; e += nwarp) {
+            const int q = nit + e;
+            if (item_t(q) / tau == k) process(q, k);
+        }
+        __syncthreads();
+        long long tb = clock64();
+        tcomp += tb - ta;
+        const int nst = s_nstep;
+        for (int e = warp; e < nst; e += nwarp) apply(e, k);
+        if (tid == 0) {
+            P.nz_count[k] = nst;
+            s_total += nst;
+        }
+        __syncthreads();
+        tapply += clock64() - tb;
+        if (s_miss && k + 1 < c) {
+            // a flagged item stepped: scan the later slots for its rows and column
+            // (key batches of at most half the miss table)
+            const int per = std::max(1, ((1 << F.mlog) / 2) / (1 + P.nrow));
+            for (int b0 = 0; b0 < nst; b0 += per) {
+                for (int w = tid; w < (1 << F.mlog); w += nth) {
+                    s_mkey[w] = -1;
+                    s_mstamp[w] = 0x7fffffff;
+                }
+                if (tid == 0) s_mcount = 0;
+                __syncthreads();
+                for (int e = b0 + tid; e < std::min(nst, b0 + per); e += nth) {
+                    const int q = e < F.scap ? s_step[e].x : -1;
+                    if (q >= 0 && q < nspec) continue;  // speculative: already tested against
+                    const int i = ld_l2_s32(P.nz_idx + k * tau + e);
+                    const int4* lanes = P.blocks + (int64_t)i * G;
+                    const int len = ld_l2_v4(lanes).y;
+                    stamp_insert(s_mkey, s_mstamp, F.mlog, i | kColKey, k);
+                    for (int ee = 0; ee < len; ++ee)
+                        stamp_insert(s_mkey, s_mstamp, F.mlog, real_row(entry(lanes, ee, false).x, P.hot_rows), k);
+                    atomicAdd(&s_mcount, 1);
+                }
+                __syncthreads();
+                if (s_mcount > 0) {
+                    test_slots(P, s_mkey, s_mstamp, F.mlog, (int64_t)(k + 1) * tau, total, tid, nth, cand + ncand,
+                               &s_nextra);
+                    if (tid == 0) ++s_nscan;
+                }
+                __syncthreads();
+            }
+            if (tid == 0) ++s_nmiss;
+        }
+        if (tid == 0) {
+            s_nstep = 0;
+            s_miss = 0;
+        }
+        __syncthreads();
+    }
+    // clear what the chunk left: spilled D rows, the item bits, the item counters
+    if (s_dspill) {
+        for (int k = 0; k < c; ++k) {
+            const int cnt = ld_l2_s32(P.nz_count + k);
+            for (int e = tid; e < cnt; e += nth) {
+                const int i = ld_l2_s32(P.nz_idx + k * tau + e);
+                const int4* lanes = P.blocks + (int64_t)i * G;
+                const int len = ld_l2_v4(lanes).y;
+                for (int ee = 0; ee < len; ++ee) P.d0[real_row(entry(lanes, ee, false).x, P.hot_rows)] = 0.0f;
+            }
+        }
+    }
+    for (int q = tid; q < nit + s_nextra; q += nth) P.bits[item_t(q) >> 5] = 0u;
+    __syncthreads();
+    if (tid == 0) {
+        P.counts[0] = 0;
+        P.counts[1] = 0;
+        P.counts[2] += s_nmiss;
+        P.counts[3] += s_nscan;
+        P.counts[4] += nspec;
+        P.counts[5] += ncand + s_nextra;
+        P.counts[6] += (int)((tclk1 - tclk0) >> 10);
+        P.counts[7] += (int)(tcomp >> 10);
+        P.counts[8] += (int)(tapply >> 10);
+        P.counts[9] += (int)((clock64() - tclk1) >> 10);
+        if (s_total) atomicAdd(P.nz_total, (unsigned long long)s_total);
+    }
+}
+
 // pass 3: one thread per slot for G <= 8 (PCDM_BATCHED_GROUP=1: one group per slot)
 template <int G>
 const void* step_kernel(bool logistic) {
@@ -626,6 +1225,36 @@ const void* step_kernel(bool logistic) {
                             : (const void*)pcdm_batched_slot_kernel<G, false>;
     }
     return logistic ? (const void*)pcdm_batched_kernel<G, true> : (const void*)pcdm_batched_kernel<G, false>;
+}
+
+// the fix-up's shared-memory shape: D map 2^13 rows, 2^11 stepped columns, 1024 steps
+// per iteration, a 2^10-key miss table; the rest stages items (PCDM_SCREEN_SMALL=1: tiny
+// maps and staging, so that tests reach the spill and global paths)
+FixShape fix_shape(const BatchedParams& P, int G) {
+    FixShape F;
+    F.nl = std::min(G, 1 + (P.nrow + 1) / 2);
+    F.c = (int)P.iters;
+    const char* sm = knob("PCDM_SCREEN_SMALL");
+    if (sm && atoi(sm) != 0) {
+        F.dlog = 4;
+        F.clog = 3;
+        F.scap = 2;
+        F.mlog = 5;
+        F.icap = 3;
+        return F;
+    }
+    F.dlog = 13;
+    F.clog = 11;
+    F.scap = 1024;
+    F.mlog = 10;
+    F.icap = 0;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t fixed = fix_smem_bytes(F) + 1024;  // + static shared memory
+    const size_t per = (size_t)16 * (1 + F.nl) + 4;
+    if ((size_t)optin > fixed) F.icap = (int)std::min<size_t>(((size_t)optin - fixed) / per, 1 << 20);
+    return F;
 }
 
 template <int G>
@@ -645,6 +1274,7 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
                                                   : (const void*)pcdm_batched_kernel<G, false>))
         P.rnv = G / 2;
     P.rnv = std::max(1, std::min(P.rnv, G / 2));
+    if (P.screen && P.logistic) P.screen = 0;  // dense steps: the grid-barrier pass
     const size_t sm1 = expand_smem<G>(P.cq_log, P.nb);
     e = cudaFuncSetAttribute(batch_expand_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     if (e != cudaSuccess) return e;
@@ -663,6 +1293,19 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
         batch_sweep_kernel<true><<<std::min(ngrp, 2 * sms), kThreads, sm2, st>>>(P, qpc);
     else
         batch_sweep_kernel<false><<<std::min(ngrp, 2 * sms), kThreads, sm2, st>>>(P, qpc);
+    if (P.screen) {
+        const size_t smt = (size_t)8 << kTestLog;
+        e = cudaFuncSetAttribute(screen_test_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt);
+        if (e != cudaSuccess) return e;
+        screen_test_kernel<G><<<sms, kTestThreads, smt, st>>>(P);
+        FixShape F = fix_shape(P, G);
+        const size_t smf = fix_smem_bytes(F);
+        e = cudaFuncSetAttribute(screen_fix_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);
+        if (e != cudaSuccess) return e;
+        screen_fix_kernel<G><<<1, kTestThreads, smf, st>>>(P, F);
+        *launches += 4;
+        return cudaGetLastError();
+    }
     void* args[] = {(void*)&P};
     const size_t sm3 = batched_step_smem(P.nhot);
     e = cudaLaunchCooperativeKernel(step_kernel<G>(P.logistic), dim3(ctas3), dim3(kThreads), args, sm3, st);

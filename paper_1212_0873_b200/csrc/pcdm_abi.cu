@@ -1100,7 +1100,20 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         const size_t o_del = o_idx + al(sizeof(int) * chunk * tau);
         const size_t o_cnt = o_del + al(sizeof(float) * chunk * tau);
         const size_t o_rec = o_cnt + al(sizeof(int) * chunk);
-        const size_t need = o_rec + al(sizeof(int2) * chunk * tau * G);
+        // SCREENED step pass (LASSO; kernels_batched.cu): per slot {L, x} + its rows,
+        // item bits and lists, in place of the grid-barrier pass's slot records
+        // (PCDM_BATCHED_SCREEN=0: the grid-barrier pass)
+        const char* scr_env = knob("PCDM_BATCHED_SCREEN");
+        const bool screen = p->loss == 0 && !(scr_env && atoi(scr_env) == 0);
+        const int64_t T = chunk * tau;
+        const int nrow = (int)std::max<int64_t>(1, p->max_len);
+        const size_t o_lx = o_rec + (screen ? 0 : al(sizeof(int2) * T * G));
+        const size_t o_rows = o_lx + (screen ? al(sizeof(int2) * T) : 0);
+        const int64_t rows_ld = (T + 3) & ~(int64_t)3;  // 16-byte row loads in the test pass
+        const size_t o_bits = o_rows + (screen ? al(sizeof(int) * rows_ld * nrow) : 0);
+        const size_t o_items = o_bits + (screen ? al(sizeof(unsigned) * ((rows_ld + 31) / 32)) : 0);
+        const size_t o_counts = o_items + (screen ? al(sizeof(int) * 3 * rows_ld) : 0);
+        const size_t need = o_counts + al(sizeof(int) * 16);
         if (p->bat_cap < need) {
             cudaFree(p->bat_mem);
             p->bat_mem = nullptr;
@@ -1130,6 +1143,18 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         B.nz_delta = (float*)(base + o_del);
         B.nz_count = (int*)(base + o_cnt);
         B.rec = (int2*)(base + o_rec);
+        B.screen = screen ? 1 : 0;
+        if (screen) {
+            B.lx = (int2*)(base + o_lx);
+            B.rows = (int*)(base + o_rows);
+            B.rows_ld = rows_ld;
+            B.nrow = nrow;
+            B.bits = (unsigned*)(base + o_bits);
+            B.items = (int*)(base + o_items);
+            CK(cudaMemsetAsync(B.bits, 0, sizeof(unsigned) * ((T + 31) / 32), st), "memset item bits");
+        }
+        B.counts = (int*)(base + o_counts);
+        CK(cudaMemsetAsync(B.counts, 0, sizeof(int) * 16, st), "memset item counts");
         B.rnv = 1 + (int)((std::max<int64_t>(p->max_len - 2, 0) + 3) / 4);  // 10 entries (huge): 3 vectors, 48 B
         B.barrier = p->sc->barrier;
         B.flags = &p->sc->flags;
@@ -1238,7 +1263,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         // launch, the packed loop keeps them (the one-barrier scheme replays list k-1)
         CK(cudaMemsetAsync(p->sc->barrier, 0, sizeof(p->sc->barrier), st), "memset barrier");
         if (!packed && !batched) CK(cudaMemsetAsync(p->sc->nz_count, 0, 3 * sizeof(int), st), "memset step lists");
-        if (batched) CK(cudaMemsetAsync(B.nz_count, 0, sizeof(int) * c, st), "memset step lists");
+        if (batched && !B.screen) CK(cudaMemsetAsync(B.nz_count, 0, sizeof(int) * c, st), "memset step lists");
         CK(tm.end(T_SAMPLER, ts), "event");
         int ti;
         CK(tm.begin(&ti), "event");
@@ -1382,6 +1407,17 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         cudaGetLastError();
     }
     stats.setup_ms = tms[T_SETUP];
+    if (B.screen && B.counts) {
+        int cnt[16] = {0};
+        CK(cudaMemcpy(cnt, B.counts, sizeof(cnt), cudaMemcpyDeviceToHost), "read screen counts");
+        stats.screen_misses = cnt[2];
+        stats.screen_scans = cnt[3];
+        stats.screen_spec = cnt[4];
+        stats.screen_flagged = cnt[5];
+        if (knob("PCDM_SCREEN_CLOCKS"))
+            fprintf(stderr, "screen clocks (kcyc): stage %d compute %d apply %d loop %d probes %d dgets %d\n", cnt[6], cnt[7],
+                    cnt[8], cnt[9], cnt[10], cnt[11]);
+    }
     p->stats = stats;
     if (hs.flags & FLAG_SAMPLER) return fail(PCDM_ESAMPLER, "sampler round counter overflow");
     if (hs.flags & FLAG_DIVERGED) return fail(PCDM_EDIVERGED, "non-finite step (diverged)");

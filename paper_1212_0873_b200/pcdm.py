@@ -44,7 +44,9 @@ class RunStats(ctypes.Structure):
                 ("iter_launches", ctypes.c_int64), ("iter_kernel_ms", ctypes.c_double),
                 ("sampler_ms", ctypes.c_double), ("setup_ms", ctypes.c_double),
                 ("hot_rows", ctypes.c_int64), ("host_h2d_bytes", ctypes.c_int64),
-                ("host_d2h_bytes", ctypes.c_int64)]
+                ("host_d2h_bytes", ctypes.c_int64), ("screen_misses", ctypes.c_int64),
+                ("screen_scans", ctypes.c_int64), ("screen_spec", ctypes.c_int64),
+                ("screen_flagged", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -158,3 +158,41 @@ def test_auto_batched_forced_fallback(gpu, monkeypatch, chunk):
     assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
     assert_parity(out)
     _check_r(out)
+
+
+# The step pass of the batched loop: the screened form (default for LASSO: speculative
+# steps from g0, a test pass, one fix-up CTA replaying the chunk over its items) against
+# the grid-barrier form (PCDM_BATCHED_SCREEN=0) and against the screened form with tiny
+# shared-memory maps (PCDM_SCREEN_SMALL=1: D spills to the dense buffer, the stepped-column
+# set overflows, items are read from global memory, steps overflow the shared list).
+@pytest.mark.parametrize("mode", ["screen", "grid", "small"])
+def test_batched_step_pass_forms(gpu, monkeypatch, mode):
+    if mode == "grid":
+        monkeypatch.setenv("PCDM_BATCHED_SCREEN", "0")
+    if mode == "small":
+        monkeypatch.setenv("PCDM_SCREEN_SMALL", "1")
+    m, n = 5000, 4000
+    rng = np.random.default_rng(13)
+    for lens in (np.full(n, 10), rng.integers(0, 15, size=n)):
+        c, r, v, b, lam = _ragged(m, n, lens, 9, lam_frac=0.05)
+        x0 = np.random.default_rng(4).normal(size=n) * (np.arange(n) % 5 == 0)
+        for tau, iters, refresh in ((64, 150, 0), (1000, 40, 7), (4000, 6, -1)):
+            out = run_both(c, r, v, b, lam, m, tau, iters, seed=tau + 1, variant="batched", x0=x0,
+                           refresh_every=refresh)
+            assert out["stats"]["variant"] == pcdm.VARIANTS["batched"]
+            assert_parity(out)
+            _check_r(out)
+            if mode != "grid" and tau == 1000:
+                # dense start: flagged slots step, so the later-slot scans run
+                assert out["stats"]["screen_misses"] > 0
+            if mode == "grid":
+                assert out["stats"]["screen_misses"] == 0
+
+
+def test_batched_screen_sparse_steps_no_misses(gpu):
+    # from x = 0 with a large lambda the speculative steps are (almost) all the steps
+    inst = I.generate(I.InstanceConfig("sparse_steps", 200_000, 20_000, 10, 100, lam_frac=0.5), seed=3)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 2000, 37, seed=3, variant="batched")
+    assert_parity(out)
+    _check_r(out)
+    assert out["stats"]["screen_misses"] <= 2
