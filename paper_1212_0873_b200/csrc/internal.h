@@ -263,13 +263,26 @@ struct BatchedParams {
     unsigned* bits;       // [ceil(rows_ld / 32)] slot is already an item (zero between chunks)
     int* items;           // [2][rows_ld]: speculative slots, then flagged slots
     int* counts;          // [4]: #speculative, #flagged, misses (run total), scans (run total)
-    int fix_cap;          // debug: cap on the fix-up's staged items / map sizes (0 = by shared memory)
+    int fix_cap;          // (unused)
+    int G;                // 16-byte chunks per column block (set by launch_batched)
+    // the previous chunk's step lists (its fix-up may still run while this chunk's expand
+    // reads x_i): the sweep re-reads x_i of the columns listed there; nullptr: none
+    const int* prev_nz_idx;
+    const int* prev_nz_count;
+    int prev_iters;
+};
+// screened pass scheduling: the fix-up runs on its own stream after the test pass
+// (ev_test) and the next chunk's sweep waits for it (ev_fix)
+struct ScreenSched {
+    cudaStream_t st2;
+    cudaEvent_t ev_test, ev_fix;
 };
 size_t batched_step_smem(int nhot);
 int batched_cq_log(int G);
 int batched_rb(int cq_log);
 int batched_ctas(int G, int sms, bool logistic, int nhot);
-cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches);
+cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches,
+                           const ScreenSched* sch = nullptr);
 
 
 

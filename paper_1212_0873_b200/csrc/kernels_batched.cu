@@ -56,6 +56,9 @@ constexpr int kSweepMaxSlots = 40 * 512;  // pass 2: slots per CTA (x 4 B of sha
 #ifndef PCDM_SWEEP_HW
 #define PCDM_SWEEP_HW 16
 #endif
+#ifndef PCDM_SWEEP_PIPE
+#define PCDM_SWEEP_PIPE 0  // pass 2: the next segment's first entries loaded ahead (measured slower)
+#endif
 #ifndef PCDM_EXPAND_U
 #define PCDM_EXPAND_U 4  // pass 1: slots per group in flight
 #endif
@@ -105,6 +108,10 @@ __device__ __forceinline__ unsigned gmask_of() {
 __device__ __forceinline__ int4 ld_blk(const BatchedParams& P, const int4* p, int t) {
     return (t == 0 && P.xlist) ? ld_l2_v4(p) : ld_stream_v4(p);
 }
+
+// multiplicative hash of a key onto 2^log buckets (the screened pass's tables and bitmaps)
+__device__ __forceinline__ uint32_t key_hash(uint32_t v, int log) { return (v * 0x9E3779B1u) >> (32 - log); }
+__device__ __forceinline__ uint32_t key_hash2(uint32_t v, int log) { return ((v ^ (v >> 15)) * 0x2C1B3C6Du) >> (32 - log); }
 
 // real row of a block entry (hot rows are stored as 0x80000000 | h, kernels_packed.cu)
 __device__ __forceinline__ int real_row(int v, const int* hrow) { return v < 0 ? hrow[v & 0x7fffffff] : v; }
@@ -160,7 +167,9 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (iv[u] >= 0) cv[u] = ld_stream_v4(P.blocks + (int64_t)iv[u] * G + t);
+            // through L2 (ld.cg): the previous chunk's fix-up may be writing x_i into the
+            // headers meanwhile (the non-coherent path requires data unchanged during the kernel)
+            if (iv[u] >= 0) cv[u] = ld_l2_v4(P.blocks + (int64_t)iv[u] * G + t);
     };
     int ivn[U];
     int4 cvn[U];
@@ -272,9 +281,32 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
 // of the group in bin-major order (a segment holds ~100 entries on `huge`: ~7 per
 // lane, all in flight); the next segment's bounds are loaded ahead.  (One CTA-wide
 // list per bin was slower: 391 vs 288 us per 18 iterations, a barrier per bin.)
+constexpr int kStaleLog = 16;  // sweep: bitmap of the columns the previous chunk stepped (8 KB)
 template <bool LOGISTIC>
 __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams P, int qpc) {
     extern __shared__ float s_g[];
+    unsigned* s_stale = (unsigned*)(s_g + (qpc << P.cq_log));
+    __shared__ int s_all_stale;
+    if (!LOGISTIC && P.screen) {
+        // the columns the previous chunk stepped: this chunk's expand may have read their
+        // x_i before that chunk's fix-up wrote it (the two overlap), so the epilogue
+        // re-reads x_i for them (all columns when there are too many steps)
+        for (int w = threadIdx.x; w < (1 << (kStaleLog - 5)); w += blockDim.x) s_stale[w] = 0u;
+        if (threadIdx.x == 0) s_all_stale = 0;
+        __syncthreads();
+        if (P.prev_nz_idx) {
+            for (int k = 0; k < P.prev_iters; ++k) {
+                const int cnt = ld_l2_s32(P.prev_nz_count + k);
+                if (cnt > 4096) s_all_stale = 1;
+                else
+                    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+                        const uint32_t h = key_hash((uint32_t)ld_l2_s32(P.prev_nz_idx + k * P.tau + e), kStaleLog);
+                        atomicOr(s_stale + (h >> 5), 1u << (h & 31));
+                    }
+            }
+        }
+        __syncthreads();
+    }
     constexpr int HW = PCDM_SWEEP_HW;  // lanes per segment
     const int hl = threadIdx.x & (HW - 1), hw = threadIdx.x / HW;
     constexpr int NH = kThreads / HW;
@@ -295,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
             lo = __ldg(offs);
             hi = __ldg(offs + 1);
         };
+#if PCDM_SWEEP_PIPE
         // the first HW * U entries of the next segment are loaded before the current
         // segment's gathers (software pipelining: one segment's entries always in flight)
         constexpr int U = 6;
@@ -353,21 +386,75 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
             nlo = n2lo;
             nhi = n2hi;
         }
+#else
+        int lo = 0, hi = 0;
+        if (hw < nseg) bounds(hw, lo, hi);
+        for (int sg = hw; sg < nseg; sg += NH) {
+            int nlo = 0, nhi = 0;
+            if (sg + NH < nseg) bounds(sg + NH, nlo, nhi);
+            const int bb = sg / nql, ql = sg - bb * nql;
+            const int2* ent = P.gent + (int64_t)(q0 + ql) * ne;
+            const float* rb = P.r + ((int64_t)bb << P.rb);
+            float* acc = s_g + (ql << P.cq_log);
+            constexpr int U = 8;
+            for (int x0 = lo + hl; x0 < hi; x0 += HW * U) {
+                int2 e[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (x0 + HW * u < hi) e[u] = ld_stream_v2(ent + x0 + HW * u);
+                float rv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (x0 + HW * u < hi) rv[u] = __ldcg(rb + (e[u].x & rmask));
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (x0 + HW * u < hi)
+                        atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
+            }
+            lo = nlo;
+            hi = nhi;
+        }
+#endif
         __syncthreads();
         float* g0 = P.g0 + ((int64_t)q0 << P.cq_log);
         const int64_t left = total - ((int64_t)q0 << P.cq_log);
-        for (int k = threadIdx.x; k < nacc && k < left; k += blockDim.x) {
-            const float g = s_g[k];
-            g0[k] = g;
-            if (!LOGISTIC && P.screen) {
-                // the speculative step: the slot's step if no earlier step of the chunk
-                // touched its rows or its column (the fix-up's arithmetic in that case, bit
-                // for bit); nonzero ones become items of the fix-up
-                const int64_t t = ((int64_t)q0 << P.cq_log) + k;
-                const int2 lx = ld_stream_v2(P.lx + t);
-                if (lx.x != -1) {
-                    const float xi = __int_as_float(lx.y);
-                    const float xp = prox_l1(xi, g, P.beta * __int_as_float(lx.x), P.lambda);
+        const int kend = (int)std::min<int64_t>(nacc, left);
+        if (LOGISTIC || !P.screen) {
+            for (int k = threadIdx.x; k < kend; k += blockDim.x) g0[k] = s_g[k];
+        } else {
+            // the speculative step of every slot: its step if no earlier step of the chunk
+            // touched its rows or its column (the fix-up's arithmetic in that case, bit for
+            // bit); nonzero ones become items of the fix-up.  Four slots per thread with
+            // their loads in flight together.
+            constexpr int EU = 4;
+            for (int k0 = threadIdx.x; k0 < kend; k0 += EU * blockDim.x) {
+                int2 lx[EU];
+                int iv[EU];
+#pragma unroll
+                for (int u = 0; u < EU; ++u) {
+                    const int k = k0 + u * blockDim.x;
+                    const int64_t t = ((int64_t)q0 << P.cq_log) + k;
+                    lx[u] = k < kend ? ld_stream_v2(P.lx + t) : make_int2(-1, 0);
+                    iv[u] = k < kend && P.prev_nz_idx ? ld_stream_s32(P.slots + t) : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < EU; ++u) {
+                    const int k = k0 + u * blockDim.x;
+                    if (k >= kend) break;
+                    const int64_t t = ((int64_t)q0 << P.cq_log) + k;
+                    const float g = s_g[k];
+                    g0[k] = g;
+                    if (lx[u].x == -1) continue;
+                    float xi = __int_as_float(lx[u].y);
+                    if (iv[u] >= 0) {
+                        // x_i may predate the previous chunk's fix-up: re-read it for the
+                        // columns that chunk stepped
+                        const uint32_t h = key_hash((uint32_t)iv[u], kStaleLog);
+                        if (s_all_stale || ((s_stale[h >> 5] >> (h & 31)) & 1u))
+                            xi = P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)iv[u] * P.G) + 2)
+                                         : ld_l2_f32(P.x + iv[u]);
+                    }
+                    const float xp = prox_l1(xi, g, P.beta * __int_as_float(lx[u].x), P.lambda);
                     if (xp - xi != 0.0f) {
                         atomicOr(P.bits + (t >> 5), 1u << (t & 31));
                         P.items[atomicAdd(P.counts, 1)] = (int)t;
@@ -713,10 +800,10 @@ __global__ void batch_fold_kernel(BatchedParams P) {
 // Same arithmetic as pass 3 per slot (g0 + corrections in fp32); items that never touch a
 // dirty row take exactly the speculative step.
 constexpr int kTestThreads = 1024;
-constexpr int kTestLog = 14;  // test key table: 2^14 {key, iteration} pairs = 128 KB
+constexpr int kTestLog = 13;    // test key table: 2^13 {key, iteration} pairs = 64 KB
+constexpr int kTestBmLog = 20;  // ... and a 2^20-bit (128 KB) one-hash bitmap of its keys
 constexpr int kColKey = (int)0x80000000;  // column keys i | 2^31 (rows are >= 0)
 
-__device__ __forceinline__ uint32_t key_hash(uint32_t v, int log) { return (v * 0x9E3779B1u) >> (32 - log); }
 
 // keep the minimum stamp per key (open addressing, linear probing; never full: the
 // callers keep the load <= 1/2)
@@ -751,25 +838,27 @@ __device__ __forceinline__ bool claim_slot(unsigned* bits, int64_t t) {
 
 // test pass over slots [t0, t1) against the keys in the table: a thread takes 4
 // consecutive slots (16-byte row loads; rows_ld is a multiple of 4), all their rows in
-// flight before the probes
+// flight, then two bits per key in the Bloom bitmap `bm` (2^bmlog bits, set for every
+// key of the table; nullptr: none) -- only a slot whose key tests positive probes the
+// table (probing every key made the pass instruction-bound, 133 us per chunk on huge;
+// with one bit per key 3 % of the slots took the divergent probe path)
 __device__ __forceinline__ void test_slots(const BatchedParams& P, const int* keys, const int* stamps, int log,
-                                           int64_t t0, int64_t t1, int64_t tid, int64_t nth, int* out,
-                                           int* out_count) {
+                                           const unsigned* bm, int bmlog, int64_t t0, int64_t t1, int64_t tid,
+                                           int64_t nth, int* out, int* out_count) {
     const int64_t tau = P.tau;
     constexpr int PB = 6;  // rows per batch of loads
+    auto maybe = [&](int key) -> unsigned {
+        if (!bm) return 1u;
+        const uint32_t h1 = key_hash((uint32_t)key, bmlog), h2 = key_hash2((uint32_t)key, bmlog);
+        return (bm[h1 >> 5] >> (h1 & 31)) & (bm[h2 >> 5] >> (h2 & 31)) & 1u;
+    };
     for (int64_t tb = (t0 & ~(int64_t)3) + 4 * tid; tb < t1; tb += 4 * nth) {
         int iv[4];
-        bool hit[4];
+        unsigned any[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            iv[u] = tb + u >= t0 && tb + u < t1 ? ld_stream_s32(P.slots + tb + u) : -1;
-            hit[u] = false;
-        }
-        const int kb = (int)(tb / tau);
-        int ks[4];
+        for (int u = 0; u < 4; ++u) iv[u] = tb + u >= t0 && tb + u < t1 ? ld_stream_s32(P.slots + tb + u) : -1;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) ks[u] = (int)((tb + u) / tau);
-        (void)kb;
+        for (int u = 0; u < 4; ++u) any[u] = iv[u] >= 0 ? maybe(iv[u] | kColKey) : 0u;
         for (int p0 = 0; p0 < P.nrow; p0 += PB) {
             int4 rv[PB];
 #pragma unroll
@@ -778,17 +867,24 @@ __device__ __forceinline__ void test_slots(const BatchedParams& P, const int* ke
                                         : make_int4(-1, -1, -1, -1);
 #pragma unroll
             for (int u = 0; u < PB; ++u) {
-                hit[0] |= rv[u].x >= 0 && stamp_find(keys, stamps, log, rv[u].x) < ks[0];
-                hit[1] |= rv[u].y >= 0 && stamp_find(keys, stamps, log, rv[u].y) < ks[1];
-                hit[2] |= rv[u].z >= 0 && stamp_find(keys, stamps, log, rv[u].z) < ks[2];
-                hit[3] |= rv[u].w >= 0 && stamp_find(keys, stamps, log, rv[u].w) < ks[3];
+                any[0] |= rv[u].x >= 0 ? maybe(rv[u].x) : 0u;
+                any[1] |= rv[u].y >= 0 ? maybe(rv[u].y) : 0u;
+                any[2] |= rv[u].z >= 0 ? maybe(rv[u].z) : 0u;
+                any[3] |= rv[u].w >= 0 ? maybe(rv[u].w) : 0u;
             }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            if (iv[u] < 0) continue;
-            const bool h = hit[u] || stamp_find(keys, stamps, log, iv[u] | kColKey) < ks[u];
-            if (h && claim_slot(P.bits, tb + u)) out[atomicAdd(out_count, 1)] = (int)(tb + u);
+            if (!any[u] || iv[u] < 0) continue;
+            // a candidate: the exact test against the stamped keys
+            const int64_t ts = tb + u;
+            const int k = (int)(ts / tau);
+            bool h = stamp_find(keys, stamps, log, iv[u] | kColKey) < k;
+            for (int p = 0; p < P.nrow && !h; ++p) {
+                const int row = ld_stream_s32(P.rows + (int64_t)p * P.rows_ld + ts);
+                h = row >= 0 && stamp_find(keys, stamps, log, row) < k;
+            }
+            if (h && claim_slot(P.bits, ts)) out[atomicAdd(out_count, 1)] = (int)ts;
         }
     }
 }
@@ -798,6 +894,7 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_test_kernel(BatchedPar
     extern __shared__ int s_kt[];
     int* keys = s_kt;
     int* stamps = s_kt + (1 << kTestLog);
+    unsigned* bm = (unsigned*)(stamps + (1 << kTestLog));  // 2^kTestBmLog bits
     __shared__ int s_kmin;
     const int t = threadIdx.x & (G - 1);
     const unsigned gm = gmask_of<G>();
@@ -806,6 +903,12 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_test_kernel(BatchedPar
     const int64_t tau = P.tau;
     const int64_t total = P.iters * tau;
     const int nspec = ld_l2_s32(P.counts);
+    auto insert = [&](int key, int k) {
+        stamp_insert(keys, stamps, kTestLog, key, k);
+        const uint32_t h1 = key_hash((uint32_t)key, kTestBmLog), h2 = key_hash2((uint32_t)key, kTestBmLog);
+        atomicOr(bm + (h1 >> 5), 1u << (h1 & 31));
+        atomicOr(bm + (h2 >> 5), 1u << (h2 & 31));
+    };
     // speculative slots per table fill (keys <= half the table)
     const int per = std::max(1, ((1 << kTestLog) / 2) / (1 + P.nrow));
     for (int b0 = 0; b0 < nspec; b0 += per) {
@@ -813,6 +916,7 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_test_kernel(BatchedPar
             keys[w] = -1;
             stamps[w] = 0x7fffffff;
         }
+        for (int w = threadIdx.x; w < (1 << (kTestBmLog - 5)); w += blockDim.x) bm[w] = 0u;
         if (threadIdx.x == 0) s_kmin = 0x7fffffff;
         __syncthreads();
         const int b1 = std::min(nspec, b0 + per);
@@ -825,17 +929,17 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_test_kernel(BatchedPar
             const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
             const int len = __shfl_sync(gm, c.y, src);
             if (t == 0) {
-                stamp_insert(keys, stamps, kTestLog, i | kColKey, k);
+                insert(i | kColKey, k);
                 atomicMin(&s_kmin, k);
             } else {
-                if (pair0 < len) stamp_insert(keys, stamps, kTestLog, real_row(c.x, P.hot_rows), k);
-                if (pair0 + 1 < len) stamp_insert(keys, stamps, kTestLog, real_row(c.z, P.hot_rows), k);
+                if (pair0 < len) insert(real_row(c.x, P.hot_rows), k);
+                if (pair0 + 1 < len) insert(real_row(c.z, P.hot_rows), k);
             }
         }
         __syncthreads();
         // slots of iterations after the earliest stamp
         const int64_t t0 = ((int64_t)s_kmin + 1) * tau;
-        test_slots(P, keys, stamps, kTestLog, t0, total, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+        test_slots(P, keys, stamps, kTestLog, bm, kTestBmLog, t0, total, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
                    (int64_t)gridDim.x * blockDim.x, P.items + P.rows_ld, P.counts + 1);
         __syncthreads();
     }
@@ -873,6 +977,7 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_fix_kernel(BatchedPara
     int* s_cur = s_start + (F.c + 1);            // [c]
     __shared__ int s_nstep, s_dcount, s_ccount, s_dspill, s_cfull, s_miss, s_nextra, s_mcount, s_total, s_nmiss,
         s_nscan;
+    __shared__ unsigned long long s_xbase;
 
     const int tid = threadIdx.x, nth = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
@@ -1114,13 +1219,7 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_fix_kernel(BatchedPara
             dadd(row, v);
             red_add_f32(P.r_out + row, v);
         }
-        if (lane == 0) {
-            mark_stepped(i);
-            if (P.xlist && P.xlist_cap > 0) {
-                const unsigned long long qq = atomicAdd(P.xlist_count, 1ull);
-                if (qq < (unsigned long long)P.xlist_cap) P.xlist[qq] = i;
-            }
-        }
+        if (lane == 0) mark_stepped(i);  // (dirty-list appends: after the loop, one atomic)
     };
 
     const int64_t total = P.iters * tau;
@@ -1169,7 +1268,7 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_fix_kernel(BatchedPara
                 }
                 __syncthreads();
                 if (s_mcount > 0) {
-                    test_slots(P, s_mkey, s_mstamp, F.mlog, (int64_t)(k + 1) * tau, total, tid, nth, cand + ncand,
+                    test_slots(P, s_mkey, s_mstamp, F.mlog, nullptr, 0, (int64_t)(k + 1) * tau, total, tid, nth, cand + ncand,
                                &s_nextra);
                     if (tid == 0) ++s_nscan;
                 }
@@ -1182,6 +1281,26 @@ __global__ void __launch_bounds__(kTestThreads, 1) screen_fix_kernel(BatchedPara
             s_miss = 0;
         }
         __syncthreads();
+    }
+    // the chunk's stepped columns onto the x dirty list: one atomic for all of them
+    if (P.xlist && P.xlist_cap > 0 && s_total > 0) {
+        if (tid == 0) {
+            s_xbase = atomicAdd(P.xlist_count, (unsigned long long)s_total);
+            int run = 0;
+            for (int k = 0; k < c; ++k) {
+                s_cur[k] = run;
+                run += ld_l2_s32(P.nz_count + k);
+            }
+        }
+        __syncthreads();
+        const unsigned long long base = s_xbase;
+        for (int k = 0; k < c; ++k) {
+            const int cnt = ld_l2_s32(P.nz_count + k);
+            for (int e = tid; e < cnt; e += nth) {
+                const unsigned long long qq = base + s_cur[k] + e;
+                if (qq < (unsigned long long)P.xlist_cap) P.xlist[qq] = ld_l2_s32(P.nz_idx + k * tau + e);
+            }
+        }
     }
     // clear what the chunk left: spilled D rows, the item bits, the item counters
     if (s_dspill) {
@@ -1265,11 +1384,13 @@ size_t expand_smem(int cq_log, int nb) {
 }
 
 template <int G>
-cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int sms, int64_t* launches) {
+cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int sms, int64_t* launches,
+                       const ScreenSched* sch) {
     cudaError_t e;
     // slot records: P.rnv 16-byte vectors (rows 2 + 4 (rnv - 1) >= max column length);
     // the G-lane-group step kernel reads G / 2
     BatchedParams P = P0;
+    P.G = G;
     if (step_kernel<G>(P.logistic) == (P.logistic ? (const void*)pcdm_batched_kernel<G, true>
                                                   : (const void*)pcdm_batched_kernel<G, false>))
         P.rnv = G / 2;
@@ -1280,11 +1401,20 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
     if (e != cudaSuccess) return e;
     int per1 = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, batch_expand_kernel<G>, kExpandThreads, sm1);
-    const int g1 = std::min(P.nq, std::max(1, per1) * sms);
+    // screened with the fix-up on its own stream: the expand leaves one SM to the previous
+    // chunk's fix-up (one CTA that needs a whole SM), else two of its persistent CTAs would
+    // start only after the fix-up and finish last
+    const int esms = P.screen && sch && sms > 1 ? sms - 1 : sms;
+    const int g1 = std::min(P.nq, std::max(1, per1) * esms);
     batch_expand_kernel<G><<<g1, kExpandThreads, sm1, st>>>(P);
+    // the sweep reads r and (for the speculative steps) x: after the previous fix-up
+    if (P.screen && sch) {
+        e = cudaStreamWaitEvent(st, sch->ev_fix, 0);
+        if (e != cudaSuccess) return e;
+    }
     // pass 2: groups of qpc slot ranges per CTA, g0 accumulated in shared memory
     const int qpc = std::max(1, std::min(kSweepMaxSlots >> P.cq_log, (P.nq + 2 * sms - 1) / (2 * sms)));
-    const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float);
+    const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float) + ((size_t)1 << (kStaleLog - 3));
     const void* sw = P.logistic ? (const void*)batch_sweep_kernel<true> : (const void*)batch_sweep_kernel<false>;
     e = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     if (e != cudaSuccess) return e;
@@ -1294,7 +1424,7 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
     else
         batch_sweep_kernel<false><<<std::min(ngrp, 2 * sms), kThreads, sm2, st>>>(P, qpc);
     if (P.screen) {
-        const size_t smt = (size_t)8 << kTestLog;
+        const size_t smt = ((size_t)8 << kTestLog) + ((size_t)1 << (kTestBmLog - 3));
         e = cudaFuncSetAttribute(screen_test_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt);
         if (e != cudaSuccess) return e;
         screen_test_kernel<G><<<sms, kTestThreads, smt, st>>>(P);
@@ -1302,7 +1432,14 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
         const size_t smf = fix_smem_bytes(F);
         e = cudaFuncSetAttribute(screen_fix_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);
         if (e != cudaSuccess) return e;
-        screen_fix_kernel<G><<<1, kTestThreads, smf, st>>>(P, F);
+        cudaStream_t sf = st;
+        if (sch) {
+            if ((e = cudaEventRecord(sch->ev_test, st)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(sch->st2, sch->ev_test, 0)) != cudaSuccess) return e;
+            sf = sch->st2;
+        }
+        screen_fix_kernel<G><<<1, kTestThreads, smf, sf>>>(P, F);
+        if (sch && (e = cudaEventRecord(sch->ev_fix, sf)) != cudaSuccess) return e;
         *launches += 4;
         return cudaGetLastError();
     }
@@ -1352,13 +1489,14 @@ int batched_ctas(int G, int sms, bool logistic, int nhot) {
     return per_sm * sms;
 }
 
-cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches) {
+cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_t st, int sms, int64_t* launches,
+                           const ScreenSched* sch) {
     switch (G) {
-        case 2: return launch_all<2>(P, ctas3, st, sms, launches);
-        case 4: return launch_all<4>(P, ctas3, st, sms, launches);
-        case 8: return launch_all<8>(P, ctas3, st, sms, launches);
-        case 16: return launch_all<16>(P, ctas3, st, sms, launches);
-        default: return launch_all<32>(P, ctas3, st, sms, launches);
+        case 2: return launch_all<2>(P, ctas3, st, sms, launches, sch);
+        case 4: return launch_all<4>(P, ctas3, st, sms, launches, sch);
+        case 8: return launch_all<8>(P, ctas3, st, sms, launches, sch);
+        case 16: return launch_all<16>(P, ctas3, st, sms, launches, sch);
+        default: return launch_all<32>(P, ctas3, st, sms, launches, sch);
     }
 }
 

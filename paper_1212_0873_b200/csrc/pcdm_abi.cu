@@ -116,6 +116,8 @@ struct pcdm_problem {
     float* d0 = nullptr;       // BATCHED: D = r_k - r_0 double buffer (zero between chunks)
     float* d1 = nullptr;
     void* bat_mem = nullptr;   // BATCHED per-chunk workspace (g0, sorted entries, offsets, lists)
+    cudaStream_t fix_st = nullptr;  // screened step pass: the fix-up's stream (high priority)
+    cudaEvent_t ev_test = nullptr, ev_fix = nullptr;
     size_t bat_cap = 0;
     int64_t max_len = 0;
     double* r64 = nullptr;
@@ -182,6 +184,11 @@ void free_problem(pcdm_problem* p) {
     cudaFree(p->d0);
     cudaFree(p->d1);
     cudaFree(p->bat_mem);
+    if (p->fix_st) {
+        cudaStreamDestroy(p->fix_st);
+        cudaEventDestroy(p->ev_test);
+        cudaEventDestroy(p->ev_fix);
+    }
     cudaFree(p->xlist);
     cudaFree(p->xlist_count);
     cudaFree(p->xbuf);
@@ -1074,8 +1081,9 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.hot_cache = p->nhot > 0 && (double)tau * (double)p->hot_max_count >= 1024.0 * (double)p->n;
     if (const char* hc = knob("PCDM_HOT_CACHE")) Q.hot_cache = p->nhot > 0 && atoi(hc) != 0;
 
-    BatchedParams B{};
+    BatchedParams B{}, B1{};  // B1: the second workspace set of the screened pass
     int bat_ctas = 0;
+    int64_t bsnap = 0, bprev_c = 0;  // screened: chunks launched, the previous chunk's iterations
     // BATCHED: iterations per snapshot (the passes' unit), its own rule independent of the
     // sampler pass size: 18 (huge: the best of 9..36 with the sampler pass held fixed,
     // profiles/r01_batched_chunk_ab.txt), at most one refresh period and the run
@@ -1113,9 +1121,17 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         const size_t o_bits = o_rows + (screen ? al(sizeof(int) * rows_ld * nrow) : 0);
         const size_t o_items = o_bits + (screen ? al(sizeof(unsigned) * ((rows_ld + 31) / 32)) : 0);
         const size_t o_counts = o_items + (screen ? al(sizeof(int) * 3 * rows_ld) : 0);
-        const size_t need = o_counts + al(sizeof(int) * 16);
+        const size_t one = al(o_counts + al(sizeof(int) * 16));
+        // screened: two workspace sets, alternating per chunk, so that chunk s's fix-up
+        // (own stream) overlaps chunk s+1's expand pass
+        const size_t need = screen ? 2 * one : one;
         if (p->bat_cap < need) {
             cudaFree(p->bat_mem);
+    if (p->fix_st) {
+        cudaStreamDestroy(p->fix_st);
+        cudaEventDestroy(p->ev_test);
+        cudaEventDestroy(p->ev_fix);
+    }
             p->bat_mem = nullptr;
             p->bat_cap = 0;
             CK(cudaMalloc(&p->bat_mem, need), "alloc batched workspace");
@@ -1166,6 +1182,32 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         B.hot_rows = p->hot_rows;
         B.nhot = p->nhot;
         B.logistic = p->loss;
+        if (screen) {
+            char* b1 = base + one;
+            B1 = B;
+            B1.g0 = (float*)(b1 + o_g0);
+            B1.gent = (int2*)(b1 + o_ent);
+            B1.offs = (int*)(b1 + o_offs);
+            B1.nz_idx = (int*)(b1 + o_idx);
+            B1.nz_delta = (float*)(b1 + o_del);
+            B1.nz_count = (int*)(b1 + o_cnt);
+            B1.lx = (int2*)(b1 + o_lx);
+            B1.rows = (int*)(b1 + o_rows);
+            B1.bits = (unsigned*)(b1 + o_bits);
+            B1.items = (int*)(b1 + o_items);
+            B1.counts = (int*)(b1 + o_counts);
+            CK(cudaMemsetAsync(B1.bits, 0, sizeof(unsigned) * ((T + 31) / 32), st), "memset item bits");
+            CK(cudaMemsetAsync(B1.counts, 0, sizeof(int) * 16, st), "memset item counts");
+            if (!p->fix_st) {
+                int least = 0, greatest = 0;  // the fix-up is on the critical path of the next sweep
+                cudaDeviceGetStreamPriorityRange(&least, &greatest);
+                CK(cudaStreamCreateWithPriority(&p->fix_st, cudaStreamNonBlocking, greatest), "fix-up stream");
+                CK(cudaEventCreateWithFlags(&p->ev_test, cudaEventDisableTiming), "event");
+                CK(cudaEventCreateWithFlags(&p->ev_fix, cudaEventDisableTiming), "event");
+            }
+            // the first chunk's sweep must not wait on a previous run's (completed) fix-up
+            CK(cudaEventRecord(p->ev_fix, st), "event");
+        }
         bat_ctas = batched_ctas(G, p->sms, p->loss == 1, p->nhot);
         plan.variant = PCDM_VARIANT_BATCHED;
         plan.lanes = G;
@@ -1232,6 +1274,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                 const double rows_per_chunk =
                     (double)*p->nz_host / (double)std::max<int64_t>(nz_at, 1) * (double)bchunk * avg_len;
                 if (rows_per_chunk > 16384.0 || knob("PCDM_BATCHED_FORCE_FALLBACK")) {
+                    if (B.screen) CK(cudaStreamWaitEvent(st, p->ev_fix, 0), "join fix-up");
                     batched = false;
                     packed = true;
                     plan = packed_plan;
@@ -1268,14 +1311,28 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         int ti;
         CK(tm.begin(&ti), "event");
         if (batched) {
-            B.slots = slots_c;
-            B.iters = c;
-            B.nq = (int)((c * tau + (1ll << B.cq_log) - 1) >> B.cq_log);
-            CK(launch_batched(p->packed_G, B, bat_ctas, st, p->sms, &launches), "batched iteration kernels");
+            BatchedParams& Bc = (B.screen && (bsnap & 1)) ? B1 : B;
+            const BatchedParams& Bo = (B.screen && (bsnap & 1)) ? B : B1;
+            Bc.slots = slots_c;
+            Bc.iters = c;
+            Bc.nq = (int)((c * tau + (1ll << Bc.cq_log) - 1) >> Bc.cq_log);
+            // screened: the x_i this chunk's expand reads may miss the previous chunk's steps
+            // (its fix-up runs beside the expand); the sweep re-reads x_i of those columns
+            Bc.prev_nz_idx = Bc.screen && bprev_c > 0 ? Bo.nz_idx : nullptr;
+            Bc.prev_nz_count = Bo.nz_count;
+            Bc.prev_iters = (int)bprev_c;
+            ScreenSched sch{};
+            if (Bc.screen) sch = ScreenSched{p->fix_st, p->ev_test, p->ev_fix};
+            CK(launch_batched(p->packed_G, Bc, bat_ctas, st, p->sms, &launches, Bc.screen ? &sch : nullptr),
+               "batched iteration kernels");
+            ++bsnap;
+            bprev_c = c;
+            cudaStream_t nz_st = Bc.screen ? p->fix_st : st;
             if (bat_fallback && !nz_pending) {
-                CK(cudaMemcpyAsync(p->nz_host, &p->sc->nz_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
+                CK(cudaMemcpyAsync(p->nz_host, &p->sc->nz_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   nz_st),
                    "read step count");
-                CK(cudaEventRecord(p->ev_nz, st), "event");
+                CK(cudaEventRecord(p->ev_nz, nz_st), "event");
                 nz_at = done + c;
                 nz_pending = true;
             }
@@ -1313,6 +1370,10 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         done += c;
         if (kernel_refresh && R > 0) stats.refreshes += (done / R) - ((done - c) / R);
         if (R > 0 && done % R == 0 && !kernel_refresh) {
+            if (B.screen) {  // the refresh reads x and r: the last fix-up first; x is current after it
+                CK(cudaStreamWaitEvent(st, p->ev_fix, 0), "join fix-up");
+                bprev_c = 0;
+            }
             int tr;
             CK(tm.begin(&tr), "event");
             float* r2 = one_barrier ? p->r2 : nullptr;
@@ -1337,6 +1398,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             ++stats.refreshes;
         }
     }
+    if (B.screen) CK(cudaStreamWaitEvent(st, p->ev_fix, 0), "join fix-up");
     p->r_cur = (one_barrier && !batched && (iters & 1)) ? p->r2 : p->r;
     int tx;
     CK(tm.begin(&tx), "event");
@@ -1408,8 +1470,10 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     }
     stats.setup_ms = tms[T_SETUP];
     if (B.screen && B.counts) {
-        int cnt[16] = {0};
+        int cnt[16] = {0}, cnt1[16] = {0};
         CK(cudaMemcpy(cnt, B.counts, sizeof(cnt), cudaMemcpyDeviceToHost), "read screen counts");
+        CK(cudaMemcpy(cnt1, B1.counts, sizeof(cnt1), cudaMemcpyDeviceToHost), "read screen counts");
+        for (int w = 0; w < 16; ++w) cnt[w] += cnt1[w];
         stats.screen_misses = cnt[2];
         stats.screen_scans = cnt[3];
         stats.screen_spec = cnt[4];
