@@ -41,7 +41,7 @@ METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
 VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", -1: "async"}
 KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
-                     5: "batch_expand+batch_sweep+pcdm_batched_slot+batch_fold",
+                     5: "batch_expand+batch_sweep+screen_test (+screen_fix on its own stream, under the next expand)",
                      -1: "pcdm_async_kernel"}
 # The oracle timing sample, per config (one definition for the cpu_baseline of our
 # arm and for every step of --impl reference): iterations k = 0..K'-1 of the

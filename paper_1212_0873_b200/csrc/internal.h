@@ -265,6 +265,7 @@ struct BatchedParams {
     int* counts;          // [4]: #speculative, #flagged, misses (run total), scans (run total)
     int fix_cap;          // (unused)
     int G;                // 16-byte chunks per column block (set by launch_batched)
+    unsigned long long* tl;  // debug timeline of the chunk's kernels (nullptr: off)
     // the previous chunk's step lists (its fix-up may still run while this chunk's expand
     // reads x_i): the sweep re-reads x_i of the columns listed there; nullptr: none
     const int* prev_nz_idx;

@@ -56,14 +56,17 @@ constexpr int kSweepMaxSlots = 40 * 512;  // pass 2: slots per CTA (x 4 B of sha
 #ifndef PCDM_SWEEP_HW
 #define PCDM_SWEEP_HW 16
 #endif
-#ifndef PCDM_SWEEP_PIPE
-#define PCDM_SWEEP_PIPE 0  // pass 2: the next segment's first entries loaded ahead (measured slower)
+#ifndef PCDM_SWEEP_ASYNC
+#define PCDM_SWEEP_ASYNC 0  // pass 2: entries through per-half-warp cp.async double buffers (measured 2.6x slower)
 #endif
 #ifndef PCDM_EXPAND_U
 #define PCDM_EXPAND_U 4  // pass 1: slots per group in flight
 #endif
 #ifndef PCDM_BATCHED_UP
 #define PCDM_BATCHED_UP 1  // pass 3: slots per thread loaded before the filter update
+#endif
+#ifndef PCDM_EXPAND_DIRECT
+#define PCDM_EXPAND_DIRECT 0  // pass 1: entries scattered straight from the staged copy (measured slower)
 #endif
 #ifndef PCDM_EXPAND_PREFETCH
 #define PCDM_EXPAND_PREFETCH 0  // pass 1: the next range's first slots loaded ahead (spills at 64 registers)
@@ -136,10 +139,28 @@ __device__ __forceinline__ bool bloom_test(const unsigned* bf, uint32_t v) {
     return (bf[a >> 5] >> (a & 31)) & (bf[b >> 5] >> (b & 31)) & 1u;
 }
 
+// debug timeline (PCDM_SCREEN_TIMELINE): per chunk and kernel, the first CTA start and
+// the last CTA end (%globaltimer ns); start stored bitwise-negated so both use atomicMax
+struct TLScope {
+    unsigned long long* p;
+    __device__ static unsigned long long now() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    }
+    __device__ TLScope(unsigned long long* tl, int k) : p(tl ? tl + 2 * k : nullptr) {
+        if (p && threadIdx.x == 0) atomicMax(p, ~now());
+    }
+    __device__ ~TLScope() {
+        if (p && threadIdx.x == 0) atomicMax(p + 1, now());
+    }
+};
+
 // ---------------------------------------------------------------- pass 1: expand + sort
 // Dynamic shared memory: stage int2[cq*maxe] | inv u16[cq*maxe] | cnt int[nb] | cur int[nb+1]
 template <int G>
 __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpandThreads) batch_expand_kernel(BatchedParams P) {
+    TLScope tl_scope(P.tl, 0);
     constexpr int MAXE = 2 * (G - 1);
     extern __shared__ int4 s_raw[];
     const int cq = 1 << P.cq_log;
@@ -237,6 +258,7 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
         }
         if (PCDM_EXPAND_PREFETCH && q + (int)gridDim.x < P.nq) load_round(q + gridDim.x, grp, ivn, cvn);
         __syncthreads();
+        int* offs = P.offs + (int64_t)q * (P.nb + 1);
         if (threadIdx.x < 32) {  // exclusive scan of the bin counts (one warp, 32 bins per step)
             int carry = 0;
             for (int b0 = 0; b0 < P.nb; b0 += 32) {
@@ -248,27 +270,39 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
                     const int y = __shfl_up_sync(0xffffffffu, incl, o);
                     if (threadIdx.x >= o) incl += y;
                 }
-                if (b < P.nb) cur[b] = carry + incl - v;
+                if (b < P.nb) {
+                    cur[b] = carry + incl - v;
+                    offs[b] = carry + incl - v;
+                }
                 carry += __shfl_sync(0xffffffffu, incl, 31);
             }
-            if (threadIdx.x == 0) cur[P.nb] = carry;
+            if (threadIdx.x == 0) {
+                cur[P.nb] = carry;
+                offs[P.nb] = carry;
+            }
         }
         __syncthreads();
-        int* offs = P.offs + (int64_t)q * (P.nb + 1);
-        for (int b = threadIdx.x; b <= P.nb; b += blockDim.x) offs[b] = cur[b];
-        __syncthreads();
+        int2* out = P.gent + (int64_t)q * ne;
+#if PCDM_EXPAND_DIRECT
+        // scatter straight to the range's output (positions from the bin cursors; the
+        // writes land within the range's 40 KB and merge in L2)
+        for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+            const int2 v = stage[e];
+            if (v.x >= 0) out[atomicAdd(cur + (v.x >> P.rb), 1)] = make_int2((v.x & rmask) | ((e / MAXE) << P.rb), v.y);
+        }
+#else
         for (int e = threadIdx.x; e < ne; e += blockDim.x) {
             const int row = stage[e].x;
             if (row >= 0) inv[atomicAdd(cur + (row >> P.rb), 1)] = (unsigned short)e;
         }
         __syncthreads();
         const int n_ent = cur[P.nb - 1];  // end of the last bin = number of entries
-        int2* out = P.gent + (int64_t)q * ne;
         for (int x = threadIdx.x; x < n_ent; x += blockDim.x) {
             const int e = inv[x];
             const int2 v = stage[e];
             out[x] = make_int2((v.x & rmask) | ((e / MAXE) << P.rb), v.y);
         }
+#endif
         __syncthreads();
     }
 }
@@ -284,8 +318,10 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
 constexpr int kStaleLog = 16;  // sweep: bitmap of the columns the previous chunk stepped (8 KB)
 template <bool LOGISTIC>
 __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams P, int qpc) {
+    TLScope tl_scope(P.tl, 1);
     extern __shared__ float s_g[];
     unsigned* s_stale = (unsigned*)(s_g + (qpc << P.cq_log));
+    int2* s_buf = (int2*)(s_stale + (1 << (kStaleLog - 5)));  // [NH][2][64] entry buffers (PCDM_SWEEP_ASYNC)
     __shared__ int s_all_stale;
     if (!LOGISTIC && P.screen) {
         // the columns the previous chunk stepped: this chunk's expand may have read their
@@ -327,64 +363,77 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
             lo = __ldg(offs);
             hi = __ldg(offs + 1);
         };
-#if PCDM_SWEEP_PIPE
-        // the first HW * U entries of the next segment are loaded before the current
-        // segment's gathers (software pipelining: one segment's entries always in flight)
-        constexpr int U = 6;
-        auto first_chunk = [&](int sg, int lo, int hi, int2 (&e)[U]) {
-            const int bb = sg / nql, ql = sg - bb * nql;
-            const int2* ent = P.gent + (int64_t)(q0 + ql) * ne;
+#if PCDM_SWEEP_ASYNC
+        // a half-warp streams its segments in chunks of CH entries through two shared
+        // buffers: the next chunk's entries are copied (cp.async) while the current chunk's
+        // rows are gathered and accumulated, so an entry load is always in flight
+        constexpr int CH = 64;
+        int2* buf = s_buf + hw * 2 * CH;
+        const unsigned hmask = HW == 32 ? 0xffffffffu : (((1u << HW) - 1u) << ((threadIdx.x & 31) & ~(HW - 1)));
+        int csg = hw, chi = 0, cpos = 0, nlo = 0, nhi = 0;
+        if (csg < nseg) bounds(csg, cpos, chi);
+        if (csg + NH < nseg) bounds(csg + NH, nlo, nhi);
+        int sg0 = 0, n0 = 0, sg1 = 0, n1 = 0;  // the chunk in each buffer
+        auto issue = [&](int slot) -> bool {
+            while (csg < nseg && cpos >= chi) {
+                csg += NH;
+                if (csg >= nseg) break;
+                cpos = nlo;
+                chi = nhi;
+                if (csg + NH < nseg) bounds(csg + NH, nlo, nhi);
+            }
+            if (csg >= nseg) {
+                if (slot) n1 = 0;
+                else n0 = 0;
+                return false;
+            }
+            const int n = min(CH, chi - cpos);
+            const int bb = csg / nql, ql = csg - bb * nql;
+            const int2* ent = P.gent + (int64_t)(q0 + ql) * ne + cpos;
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(buf + slot * CH);
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (lo + hl + HW * u < hi) e[u] = ld_stream_v2(ent + lo + hl + HW * u);
+            for (int u = 0; u < CH / HW; ++u) {
+                const int idx = hl + HW * u;
+                if (idx < n)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8 * idx), "l"(ent + idx) : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            if (slot) {
+                sg1 = csg;
+                n1 = n;
+            } else {
+                sg0 = csg;
+                n0 = n;
+            }
+            cpos += n;
+            return true;
         };
-        int lo = 0, hi = 0, nlo = 0, nhi = 0;
-        int2 ec[U];
-        if (hw < nseg) {
-            bounds(hw, lo, hi);
-            first_chunk(hw, lo, hi, ec);
-        }
-        if (hw + NH < nseg) bounds(hw + NH, nlo, nhi);
-        for (int sg = hw; sg < nseg; sg += NH) {
-            int2 en[U];
-            if (sg + NH < nseg) first_chunk(sg + NH, nlo, nhi, en);
-            int n2lo = 0, n2hi = 0;
-            if (sg + 2 * NH < nseg) bounds(sg + 2 * NH, n2lo, n2hi);
-            const int bb = sg / nql, ql = sg - bb * nql;
-            const int2* ent = P.gent + (int64_t)(q0 + ql) * ne;
+        issue(0);
+        for (int slot = 0;; slot ^= 1) {
+            const int n = slot ? n1 : n0, sgc = slot ? sg1 : sg0;
+            if (n == 0) break;
+            if (issue(slot ^ 1)) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp(hmask);
+            const int bb = sgc / nql, ql = sgc - bb * nql;
             const float* rb = P.r + ((int64_t)bb << P.rb);
             float* acc = s_g + (ql << P.cq_log);
-            {
-                float rv[U];
+            const int2* cb = buf + slot * CH;
+            int2 e[CH / HW];
+            float rv[CH / HW];
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (lo + hl + HW * u < hi) rv[u] = __ldcg(rb + (ec[u].x & rmask));
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (lo + hl + HW * u < hi)
-                        atomicAdd(acc + ((unsigned)ec[u].x >> P.rb), __int_as_float(ec[u].y) * grad_weight<LOGISTIC>(rv[u]));
-            }
-            constexpr int U2 = 4;  // the rest of a long segment (few registers: en is live)
-            for (int x0 = lo + hl + HW * U; x0 < hi; x0 += HW * U2) {
-                int2 e[U2];
-#pragma unroll
-                for (int u = 0; u < U2; ++u)
-                    if (x0 + HW * u < hi) e[u] = ld_stream_v2(ent + x0 + HW * u);
-                float rv[U2];
-#pragma unroll
-                for (int u = 0; u < U2; ++u)
-                    if (x0 + HW * u < hi) rv[u] = __ldcg(rb + (e[u].x & rmask));
-#pragma unroll
-                for (int u = 0; u < U2; ++u)
-                    if (x0 + HW * u < hi)
-                        atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
+            for (int u = 0; u < CH / HW; ++u) {
+                const int idx = hl + HW * u;
+                if (idx < n) {
+                    e[u] = cb[idx];
+                    rv[u] = __ldcg(rb + (e[u].x & rmask));
+                }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) ec[u] = en[u];
-            lo = nlo;
-            hi = nhi;
-            nlo = n2lo;
-            nhi = n2hi;
+            for (int u = 0; u < CH / HW; ++u)
+                if (hl + HW * u < n)
+                    atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
+            __syncwarp(hmask);  // the buffer is refilled next round
         }
 #else
         int lo = 0, hi = 0;
@@ -409,7 +458,11 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
 #pragma unroll
                 for (int u = 0; u < U; ++u)
                     if (x0 + HW * u < hi)
+#ifdef PCDM_SWEEP_RACY
+                        acc[(unsigned)e[u].x >> P.rb] += __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]);
+#else
                         atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
+#endif
             }
             lo = nlo;
             hi = nhi;
@@ -891,6 +944,7 @@ __device__ __forceinline__ void test_slots(const BatchedParams& P, const int* ke
 
 template <int G>
 __global__ void __launch_bounds__(kTestThreads, 1) screen_test_kernel(BatchedParams P) {
+    TLScope tl_scope(P.tl, 2);
     extern __shared__ int s_kt[];
     int* keys = s_kt;
     int* stamps = s_kt + (1 << kTestLog);
@@ -963,6 +1017,7 @@ size_t fix_smem_bytes(const FixShape& F) {
 
 template <int G>
 __global__ void __launch_bounds__(kTestThreads, 1) screen_fix_kernel(BatchedParams P, FixShape F) {
+    TLScope tl_scope(P.tl, 3);
     extern __shared__ int4 s_fix[];
     int4* s_meta = s_fix;                        // [icap] {t, i, g0, x0}
     int4* s_blk = s_meta + F.icap;               // [icap][nl] the item's block
@@ -1414,7 +1469,8 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
     }
     // pass 2: groups of qpc slot ranges per CTA, g0 accumulated in shared memory
     const int qpc = std::max(1, std::min(kSweepMaxSlots >> P.cq_log, (P.nq + 2 * sms - 1) / (2 * sms)));
-    const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float) + ((size_t)1 << (kStaleLog - 3));
+    const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float) + ((size_t)1 << (kStaleLog - 3)) +
+                       (PCDM_SWEEP_ASYNC ? (size_t)(kThreads / PCDM_SWEEP_HW) * 2 * 64 * sizeof(int2) : 0);
     const void* sw = P.logistic ? (const void*)batch_sweep_kernel<true> : (const void*)batch_sweep_kernel<false>;
     e = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     if (e != cudaSuccess) return e;

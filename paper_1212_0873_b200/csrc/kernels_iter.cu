@@ -164,11 +164,17 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
     const float beta = P.beta, lam = P.lambda;
     unsigned long long nz_total = 0;
 
+    // one slot per group (tiny: tau = 32): the next iteration's slot id is loaded at the
+    // top of this one, off the iteration's critical path
+    const bool one = tau <= ngroups;
+    int i_next = one && gid < tau && P.iters > 0 ? P.slots[gid] : -1;
     for (int64_t it = 0; it < P.iters; ++it) {
         const int* S = P.slots + it * tau;
         int* s_cnt = s_cnt2 + (it & 1);
+        const int i_cur = i_next;
+        if (one && gid < tau && it + 1 < P.iters) i_next = __ldg(P.slots + (it + 1) * tau + gid);
         for (int j = gid; j < tau; j += ngroups) {
-            const int i = S[j];
+            const int i = one ? i_cur : S[j];
             if (i < 0) continue;  // idle processor
             const int s = s_col[i], e = s_col[i + 1];
             float acc = 0.0f;

@@ -759,8 +759,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // PCDM_PRESAMPLE_DEV=0: sample in the run's stream
     const char* pe = knob("PCDM_PRESAMPLE");
     const char* pdev = knob("PCDM_PRESAMPLE_DEV");
-    const bool per_pass = pdev ? atoi(pdev) != 0 : true;
-    const bool presample = (!x_dev || per_pass) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
+    // PCDM_PRESAMPLE_JOIN=1: every pass drawn before the first iteration kernel (no overlap)
+    const char* pjoin = knob("PCDM_PRESAMPLE_JOIN");
+    const bool join_all = pjoin && atoi(pjoin) != 0;
+    const bool per_pass = (pdev ? atoi(pdev) != 0 : true) && !join_all;
+    const bool presample = (!x_dev || per_pass || join_all) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
                            !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
     // ragged layout: the slot arrays are binned by column class; with presampling the
     // binning rides on each sampler pass (side stream), else it runs before each launch
@@ -1084,6 +1087,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     BatchedParams B{}, B1{};  // B1: the second workspace set of the screened pass
     int bat_ctas = 0;
     int64_t bsnap = 0, bprev_c = 0;  // screened: chunks launched, the previous chunk's iterations
+    unsigned long long* tl_buf = nullptr;  // debug timeline (PCDM_SCREEN_TIMELINE)
+    if (knob("PCDM_SCREEN_TIMELINE")) {
+        CK(cudaMalloc((void**)&tl_buf, 8 * 256 * sizeof(unsigned long long)), "alloc timeline");
+        CK(cudaMemsetAsync(tl_buf, 0, 8 * 256 * sizeof(unsigned long long), st), "memset timeline");
+    }
     // BATCHED: iterations per snapshot (the passes' unit), its own rule independent of the
     // sampler pass size: 18 (huge: the best of 9..36 with the sampler pass held fixed,
     // profiles/r01_batched_chunk_ab.txt), at most one refresh period and the run
@@ -1291,6 +1299,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         int ts;
         CK(tm.begin(&ts), "event");
         if (!presample && done >= w1) {
+            // the window's slot buffer is reused: the last fix-up (own stream) reads it
+            if (B.screen) CK(cudaStreamWaitEvent(st, p->ev_fix, 0), "join fix-up");
             w0 = done;
             w1 = std::min(iters, done + win);
             for (int64_t s0 = w0; s0 < w1; s0 += schunk)
@@ -1321,6 +1331,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
             Bc.prev_nz_idx = Bc.screen && bprev_c > 0 ? Bo.nz_idx : nullptr;
             Bc.prev_nz_count = Bo.nz_count;
             Bc.prev_iters = (int)bprev_c;
+            if (tl_buf && bsnap < 256) Bc.tl = tl_buf + 8 * bsnap;
             ScreenSched sch{};
             if (Bc.screen) sch = ScreenSched{p->fix_st, p->ev_test, p->ev_fix};
             CK(launch_batched(p->packed_G, Bc, bat_ctas, st, p->sms, &launches, Bc.screen ? &sch : nullptr),
@@ -1481,6 +1492,20 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         if (knob("PCDM_SCREEN_CLOCKS"))
             fprintf(stderr, "screen clocks (kcyc): stage %d compute %d apply %d loop %d probes %d dgets %d\n", cnt[6], cnt[7],
                     cnt[8], cnt[9], cnt[10], cnt[11]);
+    }
+    if (tl_buf) {
+        unsigned long long h[8 * 256];
+        cudaMemcpy(h, tl_buf, sizeof(h), cudaMemcpyDeviceToHost);
+        const int ns = (int)std::min<int64_t>(bsnap, 256);
+        for (int q = 0; q < ns; ++q) {
+            const unsigned long long t0 = ~h[8 * q];
+            fprintf(stderr, "timeline chunk %d (us from expand start):", q);
+            for (int k = 0; k < 4; ++k)
+                fprintf(stderr, " [%.1f %.1f]", h[8 * q + 2 * k] ? ((double)(~h[8 * q + 2 * k]) - (double)t0) / 1e3 : -1.0,
+                        h[8 * q + 2 * k + 1] ? ((double)h[8 * q + 2 * k + 1] - (double)t0) / 1e3 : -1.0);
+            fprintf(stderr, "\n");
+        }
+        cudaFree(tl_buf);
     }
     p->stats = stats;
     if (hs.flags & FLAG_SAMPLER) return fail(PCDM_ESAMPLER, "sampler round counter overflow");
