@@ -227,14 +227,16 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config, variant, sampling, iters_per_launch):
+def ncu_traffic(config, variant, sampling, iters_per_launch, tau=None):
     """DRAM (and L2) bytes per iteration-kernel launch from the committed ncu capture of
     exactly this config, loop and sampling ("<config>:<loop>:<sampling>", written by
     tools/ncu_traffic.py), or None when that combination was not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)["%s:%s:%s" % (config, variant, sampling)]
+            table = json.load(f)
+        # a capture of this tau first ("<config>@<tau>:..."), else the config's own
+        d = table.get("%s@%s:%s:%s" % (config, tau, variant, sampling)) or table["%s:%s:%s" % (config, variant, sampling)]
     except Exception:
         return None
     out = {"dram": float(d["dram_bytes_per_iter"]) * iters_per_launch, "source": d.get("source")}
@@ -506,7 +508,7 @@ def bench_ours(args, world, rank, local):
     peak, peak_src = (L2_PEAK if r_in_l2 else (hpeak, hpeak_src))
     samp_key = args.sampling if args.sampling != "binomial" else "binomial%g" % args.p_b
     traffic = None if args.async_ else ncu_traffic(cfg.name, VARIANT_NAMES.get(st_list[-1]["variant"], "?"),
-                                                    samp_key, iters_per_launch)
+                                                    samp_key, iters_per_launch, tau)
     # ncu traffic of the bounding memory level: DRAM bytes for HBM-bound runs, L2 bytes
     # (lts__t_bytes) for L2-bound ones
     traffic_kind = ("l2" if r_in_l2 else "dram") if traffic else None

@@ -23,7 +23,7 @@ OUT = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
-def per_launch(path, regex):
+def per_launch(path, regex, total=False):
     acc = {}
     for r in load(path):
         name = r["Kernel Name"]
@@ -37,11 +37,12 @@ def per_launch(path, regex):
         rd = m.get("dram__bytes_read.sum", [0.0])
         wr = m.get("dram__bytes_write.sum", [0.0])
         l2 = m.get("lts__t_bytes.sum")
-        d = sum(rd) / len(rd) + sum(wr) / len(wr)
+        div = 1 if total else len(rd)
+        d = (sum(rd) + sum(wr)) / div
         out["dram"] += d
         out["kernels"][k] = {"dram_bytes": d, "launches": len(rd)}
         if l2:
-            out["l2"] += sum(l2) / len(l2)
+            out["l2"] += sum(l2) / (1 if total else len(l2))
     return out
 
 
@@ -52,8 +53,13 @@ def main():
     ap.add_argument("iters_per_launch", type=float)
     ap.add_argument("--kernels", default=".")
     ap.add_argument("--note", default="")
+    ap.add_argument("--total-iters", type=float, default=None,
+                    help="the capture holds every launch of runs totalling this many iterations: "
+                         "bytes summed over the launches (ITERS_PER_LAUNCH then ignored)")
     a = ap.parse_args()
-    t = per_launch(a.capture, a.kernels)
+    t = per_launch(a.capture, a.kernels, total=a.total_iters is not None)
+    if a.total_iters is not None:
+        a.iters_per_launch = a.total_iters
     d = json.load(open(OUT)) if os.path.exists(OUT) else {}
     d[a.key] = {"dram_bytes_per_iter": t["dram"] / a.iters_per_launch,
                 "l2_bytes_per_iter": (t["l2"] / a.iters_per_launch) if t["l2"] else None,
