@@ -56,20 +56,14 @@ constexpr int kSweepMaxSlots = 40 * 512;  // pass 2: slots per CTA (x 4 B of sha
 #ifndef PCDM_SWEEP_HW
 #define PCDM_SWEEP_HW 16
 #endif
-#ifndef PCDM_SWEEP_ASYNC
-#define PCDM_SWEEP_ASYNC 0  // pass 2: entries through per-half-warp cp.async double buffers (measured 2.6x slower)
-#endif
 #ifndef PCDM_EXPAND_U
 #define PCDM_EXPAND_U 4  // pass 1: slots per group in flight
 #endif
 #ifndef PCDM_BATCHED_UP
 #define PCDM_BATCHED_UP 1  // pass 3: slots per thread loaded before the filter update
 #endif
-#ifndef PCDM_EXPAND_DIRECT
-#define PCDM_EXPAND_DIRECT 0  // pass 1: entries scattered straight from the staged copy (measured slower)
-#endif
-#ifndef PCDM_EXPAND_PREFETCH
-#define PCDM_EXPAND_PREFETCH 0  // pass 1: the next range's first slots loaded ahead (spills at 64 registers)
+#ifndef PCDM_EXPAND_COALESCE
+#define PCDM_EXPAND_COALESCE 1  // pass 1: slot records staged and written coalesced after the load phase
 #endif
 #ifndef PCDM_EXPAND_MINB
 #define PCDM_EXPAND_MINB 2
@@ -161,7 +155,10 @@ struct TLScope {
 template <int G>
 __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpandThreads) batch_expand_kernel(BatchedParams P) {
     TLScope tl_scope(P.tl, 0);
-    constexpr int MAXE = 2 * (G - 1);
+    // stage stride per slot: the problem's longest column rounded up to an even count
+    // (P.maxe <= 2 (G - 1)); slot = e / MAXE by a 32-bit multiplicative inverse
+    const int MAXE = P.maxe;
+    const unsigned inv_me = 0xFFFFFFFFu / (unsigned)MAXE + 1u;
     extern __shared__ int4 s_raw[];
     const int cq = 1 << P.cq_log;
     const int ne = cq * MAXE;
@@ -169,6 +166,7 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
     unsigned short* inv = (unsigned short*)(stage + ne);
     int* cnt = (int*)(inv + ((ne + 7) & ~7));
     int* cur = cnt + P.nb;
+    int2* s_lx = (int2*)(cnt + ((2 * P.nb + 2) & ~1));  // [cq] {L, x} per slot (PCDM_EXPAND_COALESCE)
     const int t = threadIdx.x & (G - 1);
     const int grp = threadIdx.x / G;
     const unsigned gm = gmask_of<G>();
@@ -176,8 +174,7 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
     const int64_t total = P.iters * P.tau;
     const int rmask = (1 << P.rb) - 1;
 
-    // U slots per group in flight: the slot ids, then their blocks, then the entries;
-    // the first U of the next range are loaded before this range's sort and write phases
+    // U slots per group in flight: the slot ids, then their blocks, then the entries
     constexpr int U = PCDM_EXPAND_U;
     constexpr int GPC = kExpandThreads / G;  // groups per CTA
     auto load_round = [&](int q, int sl0, int (&iv)[U], int4 (&cv)[U]) {
@@ -192,24 +189,13 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
             // headers meanwhile (the non-coherent path requires data unchanged during the kernel)
             if (iv[u] >= 0) cv[u] = ld_l2_v4(P.blocks + (int64_t)iv[u] * G + t);
     };
-    int ivn[U];
-    int4 cvn[U];
-    if (PCDM_EXPAND_PREFETCH && (int)blockIdx.x < P.nq) load_round(blockIdx.x, grp, ivn, cvn);
     for (int q = blockIdx.x; q < P.nq; q += gridDim.x) {
         for (int b = threadIdx.x; b < P.nb; b += blockDim.x) cnt[b] = 0;
         __syncthreads();
         for (int sl0 = grp; sl0 < cq; sl0 += GPC * U) {
             int iv[U];
             int4 cv[U];
-            if (PCDM_EXPAND_PREFETCH && sl0 == grp) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    iv[u] = ivn[u];
-                    cv[u] = cvn[u];
-                }
-            } else {
-                load_round(q, sl0, iv, cv);
-            }
+            load_round(q, sl0, iv, cv);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int sl = sl0 + u * GPC;
@@ -231,12 +217,21 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
                         }
                     }
                 }
-                if (t > 0) {
+                if (t > 0 && 2 * (t - 1) < MAXE) {
                     const int e0 = sl * MAXE + 2 * (t - 1);
                     stage[e0] = ea;
                     stage[e0 + 1] = eb;
                 }
-                if (tt < total && P.screen) {
+                if (tt < total && P.screen && PCDM_EXPAND_COALESCE) {
+                    // {L_i, x_i} staged; the rows are the staged entries: both written
+                    // coalesced after the load phase
+                    if (t == 0) {
+                        int2 lx = make_int2(-1, 0);
+                        if (iv[u] >= 0)
+                            lx = make_int2(cv[u].x, P.xlist ? cv[u].z : __float_as_int(ld_l2_f32(P.x + iv[u])));
+                        s_lx[sl] = lx;
+                    }
+                } else if (tt < total && P.screen) {
                     // screened step pass: {L_i, x_i} per slot (L = -1 bits: idle slot) and the
                     // slot's real rows, row-major by entry (coalesced for the test pass)
                     if (t == 0) {
@@ -256,8 +251,18 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
                 }
             }
         }
-        if (PCDM_EXPAND_PREFETCH && q + (int)gridDim.x < P.nq) load_round(q + gridDim.x, grp, ivn, cvn);
         __syncthreads();
+        if (P.screen && PCDM_EXPAND_COALESCE) {
+            // the range's slot records, coalesced: {L, x} per slot and its rows row-major by
+            // entry (a warp writes 32 consecutive slots of one entry index per store)
+            const int64_t tq = (int64_t)q << P.cq_log;
+            for (int sl = threadIdx.x; sl < cq; sl += blockDim.x)
+                if (tq + sl < total) P.lx[tq + sl] = s_lx[sl];
+            for (int w = threadIdx.x; w < P.nrow * cq; w += blockDim.x) {
+                const int pp = w >> P.cq_log, sl = w & (cq - 1);
+                if (tq + sl < total) P.rows[pp * P.rows_ld + tq + sl] = stage[sl * MAXE + pp].x;
+            }
+        }
         int* offs = P.offs + (int64_t)q * (P.nb + 1);
         if (threadIdx.x < 32) {  // exclusive scan of the bin counts (one warp, 32 bins per step)
             int carry = 0;
@@ -283,14 +288,6 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
         }
         __syncthreads();
         int2* out = P.gent + (int64_t)q * ne;
-#if PCDM_EXPAND_DIRECT
-        // scatter straight to the range's output (positions from the bin cursors; the
-        // writes land within the range's 40 KB and merge in L2)
-        for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-            const int2 v = stage[e];
-            if (v.x >= 0) out[atomicAdd(cur + (v.x >> P.rb), 1)] = make_int2((v.x & rmask) | ((e / MAXE) << P.rb), v.y);
-        }
-#else
         for (int e = threadIdx.x; e < ne; e += blockDim.x) {
             const int row = stage[e].x;
             if (row >= 0) inv[atomicAdd(cur + (row >> P.rb), 1)] = (unsigned short)e;
@@ -300,9 +297,8 @@ __global__ void __launch_bounds__(kExpandThreads, PCDM_EXPAND_MINB * 512 / kExpa
         for (int x = threadIdx.x; x < n_ent; x += blockDim.x) {
             const int e = inv[x];
             const int2 v = stage[e];
-            out[x] = make_int2((v.x & rmask) | ((e / MAXE) << P.rb), v.y);
+            out[x] = make_int2((v.x & rmask) | ((int)__umulhi((unsigned)e, inv_me) << P.rb), v.y);
         }
-#endif
         __syncthreads();
     }
 }
@@ -321,7 +317,6 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
     TLScope tl_scope(P.tl, 1);
     extern __shared__ float s_g[];
     unsigned* s_stale = (unsigned*)(s_g + (qpc << P.cq_log));
-    int2* s_buf = (int2*)(s_stale + (1 << (kStaleLog - 5)));  // [NH][2][64] entry buffers (PCDM_SWEEP_ASYNC)
     __shared__ int s_all_stale;
     if (!LOGISTIC && P.screen) {
         // the columns the previous chunk stepped: this chunk's expand may have read their
@@ -363,79 +358,6 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
             lo = __ldg(offs);
             hi = __ldg(offs + 1);
         };
-#if PCDM_SWEEP_ASYNC
-        // a half-warp streams its segments in chunks of CH entries through two shared
-        // buffers: the next chunk's entries are copied (cp.async) while the current chunk's
-        // rows are gathered and accumulated, so an entry load is always in flight
-        constexpr int CH = 64;
-        int2* buf = s_buf + hw * 2 * CH;
-        const unsigned hmask = HW == 32 ? 0xffffffffu : (((1u << HW) - 1u) << ((threadIdx.x & 31) & ~(HW - 1)));
-        int csg = hw, chi = 0, cpos = 0, nlo = 0, nhi = 0;
-        if (csg < nseg) bounds(csg, cpos, chi);
-        if (csg + NH < nseg) bounds(csg + NH, nlo, nhi);
-        int sg0 = 0, n0 = 0, sg1 = 0, n1 = 0;  // the chunk in each buffer
-        auto issue = [&](int slot) -> bool {
-            while (csg < nseg && cpos >= chi) {
-                csg += NH;
-                if (csg >= nseg) break;
-                cpos = nlo;
-                chi = nhi;
-                if (csg + NH < nseg) bounds(csg + NH, nlo, nhi);
-            }
-            if (csg >= nseg) {
-                if (slot) n1 = 0;
-                else n0 = 0;
-                return false;
-            }
-            const int n = min(CH, chi - cpos);
-            const int bb = csg / nql, ql = csg - bb * nql;
-            const int2* ent = P.gent + (int64_t)(q0 + ql) * ne + cpos;
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(buf + slot * CH);
-#pragma unroll
-            for (int u = 0; u < CH / HW; ++u) {
-                const int idx = hl + HW * u;
-                if (idx < n)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8 * idx), "l"(ent + idx) : "memory");
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            if (slot) {
-                sg1 = csg;
-                n1 = n;
-            } else {
-                sg0 = csg;
-                n0 = n;
-            }
-            cpos += n;
-            return true;
-        };
-        issue(0);
-        for (int slot = 0;; slot ^= 1) {
-            const int n = slot ? n1 : n0, sgc = slot ? sg1 : sg0;
-            if (n == 0) break;
-            if (issue(slot ^ 1)) asm volatile("cp.async.wait_group 1;" ::: "memory");
-            else asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncwarp(hmask);
-            const int bb = sgc / nql, ql = sgc - bb * nql;
-            const float* rb = P.r + ((int64_t)bb << P.rb);
-            float* acc = s_g + (ql << P.cq_log);
-            const int2* cb = buf + slot * CH;
-            int2 e[CH / HW];
-            float rv[CH / HW];
-#pragma unroll
-            for (int u = 0; u < CH / HW; ++u) {
-                const int idx = hl + HW * u;
-                if (idx < n) {
-                    e[u] = cb[idx];
-                    rv[u] = __ldcg(rb + (e[u].x & rmask));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < CH / HW; ++u)
-                if (hl + HW * u < n)
-                    atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
-            __syncwarp(hmask);  // the buffer is refilled next round
-        }
-#else
         int lo = 0, hi = 0;
         if (hw < nseg) bounds(hw, lo, hi);
         for (int sg = hw; sg < nseg; sg += NH) {
@@ -458,16 +380,11 @@ __global__ void __launch_bounds__(kThreads, 2) batch_sweep_kernel(BatchedParams 
 #pragma unroll
                 for (int u = 0; u < U; ++u)
                     if (x0 + HW * u < hi)
-#ifdef PCDM_SWEEP_RACY
-                        acc[(unsigned)e[u].x >> P.rb] += __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]);
-#else
                         atomicAdd(acc + ((unsigned)e[u].x >> P.rb), __int_as_float(e[u].y) * grad_weight<LOGISTIC>(rv[u]));
-#endif
             }
             lo = nlo;
             hi = nhi;
         }
-#endif
         __syncthreads();
         float* g0 = P.g0 + ((int64_t)q0 << P.cq_log);
         const int64_t left = total - ((int64_t)q0 << P.cq_log);
@@ -1435,7 +1352,7 @@ template <int G>
 size_t expand_smem(int cq_log, int nb) {
     const size_t ne = (size_t)1 << cq_log;
     const size_t n = ne * 2 * (G - 1);
-    return n * sizeof(int2) + ((n + 7) & ~(size_t)7) * 2 + (size_t)(2 * nb + 1) * sizeof(int);
+    return n * sizeof(int2) + ((n + 7) & ~(size_t)7) * 2 + (size_t)((2 * nb + 2) & ~1) * sizeof(int) + ne * sizeof(int2);
 }
 
 template <int G>
@@ -1469,8 +1386,7 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
     }
     // pass 2: groups of qpc slot ranges per CTA, g0 accumulated in shared memory
     const int qpc = std::max(1, std::min(kSweepMaxSlots >> P.cq_log, (P.nq + 2 * sms - 1) / (2 * sms)));
-    const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float) + ((size_t)1 << (kStaleLog - 3)) +
-                       (PCDM_SWEEP_ASYNC ? (size_t)(kThreads / PCDM_SWEEP_HW) * 2 * 64 * sizeof(int2) : 0);
+    const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float) + ((size_t)1 << (kStaleLog - 3));
     const void* sw = P.logistic ? (const void*)batch_sweep_kernel<true> : (const void*)batch_sweep_kernel<false>;
     e = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     if (e != cudaSuccess) return e;

@@ -1104,7 +1104,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         const int G = p->packed_G;
         B.cq_log = batched_cq_log(G);
         B.rb = batched_rb(B.cq_log);
-        B.maxe = 2 * (G - 1);
+        // entries staged per slot: the longest column, rounded up to a whole 16-byte chunk
+        B.maxe = (int)std::min<int64_t>(2 * (G - 1), std::max<int64_t>(2, (p->max_len + 1) & ~(int64_t)1));
         B.nb = (int)((p->m + (1ll << B.rb) - 1) >> B.rb);
         const int64_t cq = 1ll << B.cq_log;
         const int64_t nq_max = (chunk * tau + cq - 1) / cq;
