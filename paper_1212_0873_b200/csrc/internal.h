@@ -127,6 +127,8 @@ struct IterLaunch {
     int variant;          // pcdm_variant actually used
     int ctas, threads, lanes;
     size_t smem;
+    int entries;          // SMEM: 0 = the two-barrier list kernel; E > 0 = the one-barrier
+                          // kernel (one slot per lane group, <= E entries per lane)
 };
 
 // ---- packed-block hot loop (kernels_packed.cu)
@@ -289,7 +291,7 @@ cudaError_t launch_batched(int G, const BatchedParams& P, int ctas3, cudaStream_
 
 // Choose the launch shape for `variant` (AUTO resolved) given problem sizes.
 IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,
-                     bool logistic = false);
+                     bool logistic = false, int64_t max_len = -1);
 cudaError_t launch_iter(const IterLaunch& L, const IterParams& P, cudaStream_t st, int64_t* launches);
 
 }  // namespace pcdm_internal

@@ -228,6 +228,215 @@ __global__ void __launch_bounds__(kSmemThreads) pcdm_smem_kernel(IterParams P) {
     if (threadIdx.x == 0 && nz_total) atomicAdd(P.nz_total, nz_total);
 }
 
+
+// ---------------------------------------------------------------- SMEM1 variant
+// The same problem placement, one slot per G-lane group (tau * G <= 1024), each lane
+// holding <= E entries of its column in registers, and ONE barrier per iteration: r is
+// double-buffered in shared memory.  Iteration k gathers from buf[k & 1] (every step
+// < k) and adds its own steps AND the previous iteration's steps (replayed from the
+// group's registers) into buf[(k + 1) & 1] (every step < k - 1), which nobody reads in
+// iteration k.  The barrier then publishes buf[(k + 1) & 1] = r_{k+1} (alg:PCD1 step 4,
+// every g_i of iteration k from r_k).  No step list, no counter atomics;
+// the group's lanes all hold the butterfly sum (bit-identical: fp addition commutes), so
+// each takes the step and scatters its own entries.  The next slot's column is loaded
+// into registers before the barrier (S and A do not depend on r).
+// The slot ids stream through a shared-memory double buffer of W-iteration windows
+// (cp.async, issued a window ahead): a global load per iteration on the critical path
+// measured ~0.6 us per iteration on tiny.
+__device__ __forceinline__ int smem1_window(int64_t tau) { return (int)max((int64_t)4, min((int64_t)64, 2048 / tau)); }
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+
+// Per column, computed once per launch: inv_i = 1/(beta L_i) (logistic: 1/(beta L_i + 2
+// lam)), 0 for an empty column, and lin_i = lam * inv_i (+inf for an empty column when
+// lam > 0).  The step is then multiplications only: LASSO x+ = sign(u) max(|u| - lin, 0),
+// u = x - g inv (prox_l1 with g/s -> g (1/s), lam/s -> lam (1/s): one rounding more
+// each; an empty column gives u = x, |u| - inf < 0 -> 0 for lam > 0 and x for lam = 0,
+// as prox_l1); logistic x+ = x - (g + 2 lam x) inv (x for a zero denominator).
+// Column n is a dummy empty column with x = inv = lin = 0 (idle slots: d = 0).
+template <bool LOGISTIC>
+__device__ __forceinline__ float step_inv(float x, float g, float inv, float lin, float lam) {
+    if (LOGISTIC) return x - (g + 2.0f * lam * x) * inv;
+    const float u = fmaf(-g, inv, x);
+    const float mag = fabsf(u) - lin;
+    if (!(mag > 0.0f)) return (mag == mag) ? 0.0f : mag;  // keep NaN visible
+    return copysignf(mag, u);
+}
+
+template <int G, int E, bool LOGISTIC>
+__global__ void __launch_bounds__(kSmemThreads) pcdm_smem1_kernel(IterParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = (int)P.m, n = (int)P.n;
+    const int nnz = (int)P.colptr[n];
+    const int tau = (int)P.tau;
+    const int iters = (int)P.iters;
+    const int W = smem1_window(tau);
+    const int WT = W * tau;
+    double* s_r64 = (double*)smem_raw;           // m (refresh scratch)
+    int* s_col = (int*)(s_r64 + m);              // n+2 (column n: the dummy)
+    int* s_row = s_col + (n + 2);                // nnz
+    float* s_val = (float*)(s_row + nnz);        // nnz
+    float* s_inv = s_val + nnz;                  // n+1
+    float* s_lin = s_inv + (n + 1);              // n+1
+    float* s_x = s_lin + (n + 1);                // n+1
+    float* s_rb = s_x + (n + 1);                 // 2 x m
+    float* s_b = s_rb + 2 * m;                   // m
+    int* s_sl = (int*)(s_b + m);                 // 2 x W x tau slot ids (a ring)
+    const float beta = P.beta, lam = P.lambda;
+
+    auto fetch_window = [&](int w, bool async) {
+        const int it0 = w * W;
+        const int cnt = min(W, iters - it0) * tau;
+        int* dst = s_sl + (w & 1) * WT;
+        const int* src = P.slots + (int64_t)it0 * tau;
+        for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+            if (async) cp_async4(dst + t, src + t);
+            else dst[t] = src[t];
+        }
+        if (async) asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int t = threadIdx.x; t <= n + 1; t += blockDim.x) s_col[t] = (int)P.colptr[min(t, n)];
+    for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
+        s_row[t] = P.rowidx[t];
+        s_val[t] = P.val[t];
+    }
+    for (int t = threadIdx.x; t <= n; t += blockDim.x) {
+        float inv = 0.0f, lin = 0.0f, xv = 0.0f;
+        if (t < n) {
+            const float sL = beta * P.L[t];
+            const float den = LOGISTIC ? sL + 2.0f * lam : sL;
+            inv = den == 0.0f ? 0.0f : 1.0f / den;
+            lin = LOGISTIC ? 0.0f : (sL == 0.0f ? (lam > 0.0f ? __int_as_float(0x7f800000) : 0.0f) : lam / sL);
+            xv = P.x[t];
+        }
+        s_inv[t] = inv;
+        s_lin[t] = lin;
+        s_x[t] = xv;
+    }
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        s_rb[t] = s_rb[m + t] = P.r[t];
+        s_b[t] = P.b ? P.b[t] : 0.0f;
+    }
+    if (iters > 0) fetch_window(0, false);
+    __syncthreads();
+
+    const int lane_g = threadIdx.x & (G - 1);
+    const int gid = threadIdx.x / G;
+    const bool active = gid < tau;
+    const int ring = 2 * WT;
+    unsigned nzc = 0;
+
+    // the current slot's column: entries (padding: row 0, value 0 -- the gathers are
+    // unconditional, fmaf(0, r, acc) = acc), 1/(beta L), lam/(beta L)
+    int crow[E];
+    float cval[E];
+    float cinv, clin;
+    int ci;
+    auto load_col = [&](int i) {
+        ci = i < 0 ? n : i;
+        const int s = s_col[ci], e = s_col[ci + 1];
+        cinv = s_inv[ci];
+        clin = s_lin[ci];
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            const int q = s + u * G + lane_g;
+            const bool ok = q < e;
+            crow[u] = ok ? s_row[q] : 0;
+            cval[u] = ok ? s_val[q] : 0.0f;
+        }
+    };
+    load_col(active && iters > 0 ? s_sl[gid] : -1);
+    int pi = n;          // the previous iteration's column and step (replayed)
+    float pd = 0.0f;
+    int until_refresh = P.R > 0 ? (int)(P.R - (P.k0 % P.R)) : -1;
+    int sp = tau + gid;  // ring position of the next iteration's slot id
+    int pos = 0, win = 0;  // it = win * W + pos
+
+    for (int it = 0; it < iters; ++it) {
+        const float* rr = s_rb + (it & 1) * m;
+        float* rw = s_rb + ((it + 1) & 1) * m;
+        float acc = 0.0f, acc2 = 0.0f;  // two chains when a lane holds many entries
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            if (E >= 4 && (u & 1)) acc2 = fmaf(cval[u], grad_weight<LOGISTIC>(rr[crow[u]]), acc2);
+            else acc = fmaf(cval[u], grad_weight<LOGISTIC>(rr[crow[u]]), acc);
+        }
+        acc += acc2;
+        const float xi = s_x[ci];
+        const int ni = (active && it + 1 < iters) ? s_sl[sp] : -1;
+        sp += tau;
+        if (sp >= ring) sp -= ring;
+        // window win+1 into the ring half window win-1 used (its last id was read in
+        // iteration win*W - 2, before the last barrier)
+        if (pos == 0 && (win + 1) * W < iters) fetch_window(win + 1, true);
+        // the previous iteration's step into the buffer that lacks it (rare)
+        if (pd != 0.0f) {
+            const int s = s_col[pi], e = s_col[pi + 1];
+            for (int q = s + lane_g; q < e; q += G) atomicAdd(rw + s_row[q], s_val[q] * pd);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const float xp = step_inv<LOGISTIC>(xi, acc, cinv, clin, lam);
+        const float d = xp - xi;
+        if (d != 0.0f) {  // rare for LASSO
+            if (lane_g == 0) {
+                if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
+                s_x[ci] = xp;
+                ++nzc;
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u)
+                if (cval[u] != 0.0f) atomicAdd(rw + crow[u], cval[u] * d);
+        }
+        pi = ci;
+        pd = d;
+        load_col(ni);  // S and A do not depend on r
+        if (++pos == W) pos = 0, ++win;
+        // the next window's copies land before the barrier that precedes its first read
+        if (pos == W - 1) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (--until_refresh == 0) {
+            // residual refresh (R8): r = fp32(A x - b), fp64 accumulation; both buffers
+            // then hold r_{k+1}, so nothing is replayed.  A warp takes 32 columns at a
+            // time and walks the entries of the nonzero ones.
+            until_refresh = (int)P.R;
+            pd = 0.0f;
+            for (int t = threadIdx.x; t < m; t += blockDim.x) s_r64[t] = -(double)s_b[t];
+            __syncthreads();
+            const int lane = threadIdx.x & 31;
+            for (int base = (threadIdx.x >> 5) * 32; base < n; base += (blockDim.x >> 5) * 32) {
+                const float xl = base + lane < n ? s_x[base + lane] : 0.0f;
+                unsigned nzm = __ballot_sync(0xffffffffu, xl != 0.0f);
+                while (nzm) {
+                    const int j = __ffs(nzm) - 1;
+                    nzm &= nzm - 1;
+                    const double xj = (double)__shfl_sync(0xffffffffu, xl, j);
+                    const int i = base + j;
+                    for (int q = s_col[i] + lane; q < s_col[i + 1]; q += 32)
+                        atomicAdd(s_r64 + s_row[q], (double)s_val[q] * xj);
+                }
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < m; t += blockDim.x) s_rb[t] = s_rb[m + t] = (float)s_r64[t];
+            __syncthreads();
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const float* rf = s_rb + (iters & 1) * m;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) P.x[t] = s_x[t];
+    for (int t = threadIdx.x; t < m; t += blockDim.x) P.r[t] = rf[t];
+    if (nzc) atomicAdd(P.nz_total, (unsigned long long)nzc);
+}
+
+size_t smem1_bytes(int64_t m, int64_t n, int64_t nnz, int64_t tau) {
+    const int64_t W = std::max<int64_t>(4, std::min<int64_t>(64, 2048 / std::max<int64_t>(tau, 1)));
+    return (size_t)m * 8 + (size_t)(n + 2) * 4 + (size_t)nnz * 8 + (size_t)(n + 1) * 12 + (size_t)m * 12 +
+           (size_t)(2 * W * tau) * 4;
+}
+
 size_t smem_bytes(int64_t m, int64_t n, int64_t nnz, int64_t tau) {
     return (size_t)(n + 1) * 4 + (size_t)nnz * 8 + (size_t)n * 8 + (size_t)m * 4 + (size_t)tau * 8 + 8 +
            (size_t)m * 8;  // + the refresh scratch
@@ -262,6 +471,33 @@ cudaError_t launch_lanes(const IterLaunch& L, const IterParams& P, cudaStream_t 
     }
 }
 
+template <int G, int E, bool LOG>
+cudaError_t launch_smem1(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(pcdm_smem1_kernel<G, E, LOG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L.smem);
+    if (e != cudaSuccess) return e;
+    pcdm_smem1_kernel<G, E, LOG><<<1, L.threads, L.smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+template <int E, bool LOG>
+cudaError_t launch_smem1_lanes(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
+    switch (L.lanes) {
+        case 1: return launch_smem1<1, E, LOG>(L, P, st);
+        case 2: return launch_smem1<2, E, LOG>(L, P, st);
+        case 4: return launch_smem1<4, E, LOG>(L, P, st);
+        case 8: return launch_smem1<8, E, LOG>(L, P, st);
+        case 16: return launch_smem1<16, E, LOG>(L, P, st);
+        default: return launch_smem1<32, E, LOG>(L, P, st);
+    }
+}
+
+// E > 4 entries per lane: one or two lanes per column
+template <int E, bool LOG>
+cudaError_t launch_smem1_few(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
+    return L.lanes == 1 ? launch_smem1<1, E, LOG>(L, P, st) : launch_smem1<2, E, LOG>(L, P, st);
+}
+
 template <int G, bool LOG>
 cudaError_t launch_smem(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(pcdm_smem_kernel<G, LOG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -278,6 +514,18 @@ namespace {
 template <bool LOG>
 cudaError_t launch_iter_loss(const IterLaunch& L, const IterParams& P, cudaStream_t st) {
     constexpr int kU = 8;
+    if (L.variant == 2 && L.entries > 0) {
+        switch (L.entries) {
+            case 1: return launch_smem1_lanes<1, LOG>(L, P, st);
+            case 2: return launch_smem1_lanes<2, LOG>(L, P, st);
+            case 3: return launch_smem1_lanes<3, LOG>(L, P, st);
+            case 4: return launch_smem1_lanes<4, LOG>(L, P, st);
+            case 6: return launch_smem1_few<6, LOG>(L, P, st);
+            case 8: return launch_smem1_few<8, LOG>(L, P, st);
+            case 12: return launch_smem1_few<12, LOG>(L, P, st);
+            default: return launch_smem1_few<16, LOG>(L, P, st);
+        }
+    }
     if (L.variant == 2) {
         switch (L.lanes) {
             case 1: return launch_smem<1, LOG>(L, P, st);
@@ -300,7 +548,7 @@ constexpr int kUnroll = 8;
 constexpr size_t kSmemLimit = 200 * 1024;
 
 IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau, int sms, int device,
-                     bool logistic) {
+                     bool logistic, int64_t max_len) {
     IterLaunch L{};
     const int64_t avg = (nnz + n - 1) / n;
     const size_t sm = smem_bytes(m, n, nnz, tau);
@@ -314,6 +562,28 @@ IterLaunch plan_iter(int variant, int64_t m, int64_t n, int64_t nnz, int64_t tau
         // as many threads as the slots need (each __syncthreads waits for all of them)
         L.threads = std::max(64, std::min(kSmemThreads, pow2_clamp(tau * L.lanes, 64, kSmemThreads)));
         L.smem = sm;
+        // the one-barrier kernel: one slot per group of G lanes (tau * G <= 1024 threads),
+        // the longest column in E = ceil(max_len / G) entries per lane (E <= 4, or
+        // E in {6, 8, 12, 16} for G <= 2); the most lanes that fit (E = 1 when tau allows):
+        // fewer lanes shorten the butterfly but serialise the scatter of a nonzero step and
+        // the refresh (tiny: G = 16 0.45, 4 0.52, 2 0.66, 1 1.13 us per iteration,
+        // profiles/r02_smem1_ab.txt); PCDM_SMEM1=0 keeps the two-barrier list kernel
+        // (A/B, tests), PCDM_SMEM_LANES forces G
+        const char* s1 = knob("PCDM_SMEM1");
+        const size_t sm1 = smem1_bytes(m, n, nnz, tau);
+        if (max_len >= 0 && !(s1 && atoi(s1) == 0) && sm1 <= kSmemLimit) {
+            int G = pow2_clamp(std::max<int64_t>(max_len, 1), 1, 32);
+            while (G > 1 && tau * G > kSmemThreads) G >>= 1;
+            if (const char* sl = knob("PCDM_SMEM_LANES")) G = pow2_clamp(atoi(sl), 1, 32);
+            int64_t E = std::max<int64_t>(1, (max_len + G - 1) / G);
+            if (E > 4) E = G > 2 ? 0 : E <= 6 ? 6 : E <= 8 ? 8 : E <= 12 ? 12 : E <= 16 ? 16 : 0;
+            if (E > 0 && tau * G <= kSmemThreads) {
+                L.entries = (int)E;
+                L.lanes = G;
+                L.threads = std::max(32, (int)((tau * G + 31) / 32 * 32));
+                L.smem = sm1;
+            }
+        }
         return L;
     }
     L.lanes = pow2_clamp((avg + kUnroll - 1) / kUnroll, 1, 32);

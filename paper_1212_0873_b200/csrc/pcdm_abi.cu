@@ -768,7 +768,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // ragged layout: the slot arrays are binned by column class; with presampling the
     // binning rides on each sampler pass (side stream), else it runs before each launch
     const IterLaunch plan0 = plan_iter(variant >= PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n,
-                                       p->nnz, tau, p->sms, p->device, p->loss == 1);
+                                       p->nnz, tau, p->sms, p->device, p->loss == 1, p->max_len);
     const bool ragged_plan = p->ragged && (variant == PCDM_VARIANT_PACKED ||
                                            (variant == PCDM_VARIANT_AUTO && plan0.variant == PCDM_VARIANT_GRID));
     auto ensure_bins = [&](int64_t its, int64_t scr_its) -> pcdm_status {

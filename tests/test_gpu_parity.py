@@ -107,6 +107,27 @@ def test_tiny_config_full_run(gpu, variant):
     assert out["F_orc"] < 0.5 * float((inst.b.double() ** 2).sum())
 
 
+@pytest.mark.parametrize("form", [("1", "1"), ("1", "2"), ("1", "4"), ("1", "8"), ("1", "16"), ("1", "32"), ("0", "16")])
+def test_smem_one_barrier_kernel(gpu, monkeypatch, form):
+    # the shared-memory loop: the one-barrier kernel (double-buffered r, the previous
+    # step replayed from its column) with E = 12, 6, 3, 2, 1, 1 entries per lane, and the
+    # two-barrier list kernel (PCDM_SMEM1=0); full tiny run, then a nonzero start with
+    # a refresh after every 3rd iteration (the replay is dropped at each refresh)
+    monkeypatch.setenv("PCDM_SMEM1", form[0])
+    monkeypatch.setenv("PCDM_SMEM_LANES", form[1])
+    inst = I.generate("tiny", seed=0)
+    out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 32, 2000, seed=0,
+                   variant="smem")
+    assert_parity(out)
+    c, r, v, b, lam = _ragged(600, 250, np.random.default_rng(3).integers(0, 13, size=250), 8)
+    for tau in (1, 5, 64):
+        out = run_both(c, r, v, b, lam, 600, tau, 90, seed=tau, variant="smem", refresh_every=3,
+                       x0=np.random.default_rng(5).normal(size=250))
+        assert_parity(out)
+        assert out["stats"]["refreshes"] == 30
+        np.testing.assert_allclose(out["r_gpu"], out["res"].r, rtol=0, atol=1e-4 * np.max(np.abs(out["res"].r)))
+
+
 def test_medium_config_full_run(gpu):
     inst = I.generate("medium", seed=0)
     out = run_both(inst.colptr, inst.rowidx, inst.val, inst.b, inst.lam, inst.m, 1024, 10_000, seed=0,
