@@ -19,7 +19,9 @@ struct DevCSC {
 };
 
 // ---- setup / occasional kernels (kernels_setup.cu)
-cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches);
+// L != nullptr: the same pass also writes L_i = ||a_i||^2 (fp64 sums) for valid column tiles
+cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches,
+                            float* L = nullptr);
 cudaError_t launch_check_finite(int64_t count, const float* v, int flag_bit, int* flags, cudaStream_t st,
                                 int sms, int64_t* launches);
 cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int sms, int64_t* launches);

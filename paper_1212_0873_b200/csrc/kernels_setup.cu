@@ -4,6 +4,7 @@
 //   the objective F = 1/2||r||^2 + lambda||x||_1 (eq:P).
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
 
@@ -66,11 +67,55 @@ __device__ __forceinline__ int tile_col(long long p, long long b) {
     return k;
 }
 
+// L_i = sum_p val_p^2 on column tiles: fp64 segmented warp sums (entries of a column are
+// consecutive lanes), one fp64 accumulator per tile column in shared memory (acc[32]).
+__device__ __forceinline__ void tile_norms_scan(const float* __restrict__ val, int64_t n, int64_t i0, long long b,
+                                                long long e32, double* acc, float* __restrict__ L) {
+    const int lane = threadIdx.x & 31;
+    acc[lane] = 0.0;
+    __syncwarp();
+    const long long s = __shfl_sync(0xffffffffu, b, 0);
+    for (long long p0 = s; p0 < e32; p0 += 32) {
+        const long long p = p0 + lane;
+        const bool valid = p < e32;
+        const double v = valid ? (double)ld_stream_f32(val + p) : 0.0;
+        const int kt = tile_col(p, b);  // all lanes (shuffles)
+        const int k = valid ? kt : 32;
+        double sum = v * v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan (keys non-decreasing)
+            const double y = __shfl_up_sync(0xffffffffu, sum, o);
+            const int ky = __shfl_up_sync(0xffffffffu, k, o);
+            if (lane >= o && ky == k) sum += y;
+        }
+        const int kn = __shfl_down_sync(0xffffffffu, k, 1);
+        if (valid && (lane == 31 || kn != k)) acc[k] += sum;  // the segment's last lane
+        __syncwarp();
+    }
+    if (i0 + lane < n) L[i0 + lane] = (float)acc[lane];
+    __syncwarp();
+}
+
+__global__ void col_norms_tile_kernel(int64_t n, const long long* __restrict__ colptr, const float* __restrict__ val,
+                                      float* __restrict__ L) {
+    __shared__ double s_acc[kThreads];
+    double* acc = s_acc + (threadIdx.x & ~31);
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
+        long long e32;
+        const long long b = tile_bounds(colptr, n, i0, &e32);
+        tile_norms_scan(val, n, i0, b, e32, acc, L);
+    }
+}
+
 // CSC validation on column tiles: colptr monotone and within [0, nnz], rows in [0, m)
 // and strictly increasing within a column, values finite.
 __global__ void validate_tile_kernel(int64_t m, int64_t n, int64_t nnz, const long long* __restrict__ colptr,
                                      const int* __restrict__ rowidx, const float* __restrict__ val,
-                                     int* __restrict__ flags) {
+                                     int* __restrict__ flags, float* __restrict__ L) {
+    __shared__ double s_acc[kThreads];
+    double* acc = s_acc + (threadIdx.x & ~31);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -98,46 +143,25 @@ __global__ void validate_tile_kernel(int64_t m, int64_t n, int64_t nnz, const lo
                 if (!isfinite(val[p])) bad |= FLAG_NONFINITE_VAL;
             }
         }
+        if (L) {
+            // L_i = sum val^2 (fp64) of the tile's columns, read again while the tile is in
+            // L2: a lane per column when the tile's columns are short (no shuffles), the
+            // segmented warp scan otherwise
+            const int len = (int)min(next - b, (long long)INT_MAX);
+            if (__reduce_max_sync(0xffffffffu, len) <= 64) {
+                double sum = 0.0;
+                for (long long p = b; p < next; ++p) {
+                    const double v = (double)val[p];
+                    sum = fma(v, v, sum);
+                }
+                if (i0 + lane < n) L[i0 + lane] = (float)sum;
+            } else {
+                tile_norms_scan(val, n, i0, b, e32, acc, L);
+            }
+        }
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (lane == 0 && bad) atomicOr(flags, bad);
-}
-
-// L_i = sum_p val_p^2 on column tiles: fp64 segmented warp sums (entries of a column are
-// consecutive lanes), one fp64 accumulator per tile column in shared memory.
-__global__ void col_norms_tile_kernel(int64_t n, const long long* __restrict__ colptr, const float* __restrict__ val,
-                                      float* __restrict__ L) {
-    __shared__ double s_acc[kThreads];
-    const int lane = threadIdx.x & 31;
-    double* acc = s_acc + (threadIdx.x & ~31);
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i0 = warp * 32; i0 < n; i0 += nwarps * 32) {
-        long long e32;
-        const long long b = tile_bounds(colptr, n, i0, &e32);
-        acc[lane] = 0.0;
-        __syncwarp();
-        const long long s = __shfl_sync(0xffffffffu, b, 0);
-        for (long long p0 = s; p0 < e32; p0 += 32) {
-            const long long p = p0 + lane;
-            const bool valid = p < e32;
-            const double v = valid ? (double)ld_stream_f32(val + p) : 0.0;
-            const int kt = tile_col(p, b);  // all lanes (shuffles)
-            const int k = valid ? kt : 32;
-            double sum = v * v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan (keys non-decreasing)
-                const double y = __shfl_up_sync(0xffffffffu, sum, o);
-                const int ky = __shfl_up_sync(0xffffffffu, k, o);
-                if (lane >= o && ky == k) sum += y;
-            }
-            const int kn = __shfl_down_sync(0xffffffffu, k, 1);
-            if (valid && (lane == 31 || kn != k)) acc[k] += sum;  // the segment's last lane
-            __syncwarp();
-        }
-        if (i0 + lane < n) L[i0 + lane] = (float)acc[lane];
-        __syncwarp();
-    }
 }
 
 // counts[row]++ restricted to rows in [lo, hi): the row range's counters stay in L2
@@ -161,6 +185,45 @@ __global__ void row_counts_range_kernel(int64_t nnz, const int* __restrict__ row
         const int r = rowidx[p];
         if (r >= lo && r < hi) atomicAdd(counts + r, 1);
     }
+}
+
+// Byte counters: counts of rows [lo, hi) as 8-bit fields of 32-bit words (4 rows per word,
+// a 2^26-row range in 64 MB of L2), atomicAdd of 1 << 8 (r & 3); a field that was 255
+// before the add has carried into its neighbour: *overflow is set and the caller recounts
+// with 32-bit counters (a row with more than 255 stored entries).
+__global__ void row_counts_u8_kernel(int64_t nnz, const int* __restrict__ rowidx, int lo, int hi,
+                                     unsigned* __restrict__ words, int* __restrict__ overflow) {
+    const int64_t nv = nnz / 4;
+    const int4* r4 = (const int4*)rowidx;
+    bool ovf = false;
+    auto count = [&](int r) {
+        if (r >= lo && r < hi) {
+            const int q = r - lo;
+            const unsigned sh = 8u * (unsigned)(q & 3);
+            const unsigned old = atomicAdd(words + (q >> 2), 1u << sh);
+            ovf |= ((old >> sh) & 0xFFu) == 0xFFu;
+        }
+    };
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nv; q += (int64_t)gridDim.x * blockDim.x) {
+        int4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(r4 + q));
+        count(v.x);
+        count(v.y);
+        count(v.z);
+        count(v.w);
+    }
+    for (int64_t p = nv * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (int64_t)gridDim.x * blockDim.x)
+        count(rowidx[p]);
+    if (__any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicExch(overflow, 1);
+}
+
+// counts[lo + t] = byte t of the range's words
+__global__ void row_counts_expand_kernel(int lo, int cnt, const unsigned* __restrict__ words, int* __restrict__ counts) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x)
+        counts[lo + t] = (int)((words[t >> 2] >> (8u * (unsigned)(t & 3))) & 0xFFu);
 }
 
 __global__ void check_finite_kernel(int64_t count, const float* __restrict__ v, int flag_bit,
@@ -407,10 +470,10 @@ cudaError_t launch_objective_logistic(int64_t m, int64_t n, const double* s64, c
 }
 
 
-cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches) {
+cudaError_t launch_validate(const DevCSC& A, int* flags, cudaStream_t st, int sms, int64_t* launches, float* L) {
     const int blocks = grid_for(A.n, kThreads, sms * 16);  // a warp per 32-column tile
     validate_tile_kernel<<<blocks, kThreads, 0, st>>>(A.m, A.n, A.nnz, (const long long*)A.colptr, A.rowidx,
-                                                      A.val, flags);
+                                                      A.val, flags, L);
     ++*launches;
     return cudaGetLastError();
 }
@@ -436,6 +499,33 @@ cudaError_t launch_row_counts(const DevCSC& A, int* counts, cudaStream_t st, int
         return cudaGetLastError();
     }
     const int blocks = grid_for(A.nnz / 4 + 1, kThreads, sms * 8);
+    // byte counters first: 2^26 rows per pass (huge: 2 passes instead of 6; 53 -> see
+    // profiles/r02_create_ab.txt), 32-bit counters again if a row overflowed a byte
+    const int64_t tile8 = (int64_t)1 << 26;
+    unsigned* words = nullptr;
+    int* ovf = nullptr;
+    if (cudaMalloc((void**)&words, sizeof(unsigned) * (size_t)(std::min(A.m, tile8) / 4 + 1) + 16) == cudaSuccess) {
+        ovf = (int*)(words + std::min(A.m, tile8) / 4 + 1);
+        int h_ovf = 0;
+        e = cudaMemsetAsync(ovf, 0, sizeof(int), st);
+        for (int64_t lo = 0; e == cudaSuccess && lo < A.m; lo += tile8) {
+            const int cnt = (int)std::min(tile8, A.m - lo);
+            e = cudaMemsetAsync(words, 0, sizeof(unsigned) * (size_t)(cnt / 4 + 1), st);
+            if (e != cudaSuccess) break;
+            row_counts_u8_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, (int)lo, (int)(lo + cnt), words, ovf);
+            row_counts_expand_kernel<<<grid_for(cnt, kThreads, sms * 8), kThreads, 0, st>>>((int)lo, cnt, words, counts);
+            *launches += 2;
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        cudaFree(words);
+        if (e != cudaSuccess) return e;
+        if (!h_ovf) return cudaSuccess;
+        if ((e = cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)A.m, st)) != cudaSuccess) return e;
+    } else {
+        cudaGetLastError();  // no room for the byte counters: 32-bit passes
+    }
     for (int64_t lo = 0; lo < A.m; lo += tile) {
         row_counts_range_kernel<<<blocks, kThreads, 0, st>>>(A.nnz, A.rowidx, (int)lo, (int)std::min(A.m, lo + tile),
                                                              counts);

@@ -574,7 +574,9 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
         cudaError_t e;
         if ((e = cudaMalloc((void**)&p->sc, sizeof(Scalars))) != cudaSuccess) { s = cuda_fail(e, "scalars"); break; }
         if ((e = cudaMemsetAsync(p->sc, 0, sizeof(Scalars), st)) != cudaSuccess) { s = cuda_fail(e, "memset"); break; }
-        if ((e = launch_validate(p->csc(), &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "validate"); break; }
+        // validation and the column norms L_i (a1) in one pass over the tiles of A
+        if ((e = cudaMalloc((void**)&p->L, sizeof(float) * n)) != cudaSuccess) { s = cuda_fail(e, "alloc L"); break; }
+        if ((e = launch_validate(p->csc(), &p->sc->flags, st, p->sms, &launches, p->L)) != cudaSuccess) { s = cuda_fail(e, "validate"); break; }
         if (loss == 0) {
             if ((e = launch_check_finite(m, p->b, FLAG_NONFINITE_B, &p->sc->flags, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "check b"); break; }
         } else {
@@ -588,8 +590,6 @@ pcdm_status create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* colptr
                      (loss && (hs.flags & FLAG_NONFINITE_B)) ? "labels y must be +1 or -1" : flag_text(hs.flags));
             break;
         }
-        if ((e = cudaMalloc((void**)&p->L, sizeof(float) * n)) != cudaSuccess) { s = cuda_fail(e, "alloc L"); break; }
-        if ((e = launch_col_norms(p->csc(), p->L, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "col norms"); break; }
         if (loss == 1 && (e = launch_scale(n, 0.25f, p->L, st, p->sms, &launches)) != cudaSuccess) { s = cuda_fail(e, "L"); break; }
         int* counts = nullptr;
         if ((e = cudaMalloc((void**)&counts, sizeof(int) * m)) != cudaSuccess) { s = cuda_fail(e, "alloc counts"); break; }

@@ -95,6 +95,41 @@ def test_omega_L_counts(gpu, cfg):
     prob.close()
 
 
+@pytest.mark.parametrize("hot_count", [255, 256])
+def test_row_counts_byte_counters_and_fallback(gpu, hot_count):
+    # m > 2^26: two passes of byte counters (rows [0, 2^26) and [2^26, m)); a row stored
+    # 255 times stays on them, 256 times overflows a byte and the 32-bit passes recount
+    m, n, per = (1 << 26) + 4099, 2000, 40
+    rng = np.random.default_rng(11)
+    hot = (1 << 26) + 3
+    cols = []
+    for i in range(n):
+        rows = np.unique(rng.integers(0, m, size=per))
+        extra = [m - 1, (1 << 26) - 1, 1 << 26] if i % 7 == 0 else []
+        if i < hot_count:
+            extra.append(hot)
+        cols.append(np.unique(np.concatenate([rows, np.array(extra, dtype=np.int64)])))
+    lens = np.array([len(c) for c in cols])
+    colptr = np.zeros(n + 1, dtype=np.int64)
+    colptr[1:] = np.cumsum(lens)
+    rowidx = np.concatenate(cols).astype(np.int32)
+    val = rng.normal(size=rowidx.size).astype(np.float32)
+    b = np.zeros(m, dtype=np.float32)
+    dev = gpu
+    prob = pcdm.Problem(m, n, torch.as_tensor(colptr, device=dev), torch.as_tensor(rowidx, device=dev),
+                        torch.as_tensor(val, device=dev), torch.as_tensor(b, device=dev), 0.1)
+    counts_o = oracle.row_counts(m, rowidx)
+    assert counts_o[hot] == hot_count
+    assert prob.omega == oracle.omega(m, rowidx) == int(counts_o.max())
+    counts = torch.zeros(m, dtype=torch.int32, device=dev)
+    prob.row_counts(counts)
+    assert np.array_equal(to_host(counts), counts_o)
+    L = torch.zeros(n, dtype=torch.float32, device=dev)
+    prob.col_norms(L)
+    np.testing.assert_allclose(to_host(L), oracle.col_norms(colptr, val).astype(np.float32), rtol=2e-7, atol=0)
+    prob.close()
+
+
 # ------------------------------------------------------------------ full runs
 @pytest.mark.parametrize("variant", ["auto", "smem", "block", "grid"])
 def test_tiny_config_full_run(gpu, variant):
