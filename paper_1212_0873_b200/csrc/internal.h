@@ -168,6 +168,8 @@ struct PackedParams {
                           //    cp.async.bulk (TMA engine) pieces, scattered from the staged copy
     int hot_stage;        // 1 (one-barrier scheme): scatters into hot rows accumulate in shared
                           //    memory per CTA, one red.global.add per hot row and CTA per iteration
+    int reg_replay;       // 1 (one-barrier scheme, grid covers tau in one round): pcdm_packed1_kernel,
+                          //    the previous step replayed from the registers of the group that took it
     // ragged layout (kernels_ragged.cu): per iteration the slots binned by class
     const int2* bins;     // [iters][tau] {i, chunk offset of column i}, grouped by class
     const int* bcnt;      // [iters][8] class starts (2, 4, 8, 16, 32 lanes, warp-long, CTA-long) and end

@@ -327,6 +327,140 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
     }
 }
 
+// ---------------------------------------------------------------- one slot per group
+// The one-barrier loop for grids that cover tau in one round (every group of G lanes owns
+// at most one slot per iteration: the small-tau, latency-bound configs).  The group that
+// took the step of iteration k-1 still holds that column's chunk and delta in registers,
+// so the replay of Delta_{k-1} into Q needs no step list: no list counter to read after
+// the barrier, no dependent list and block loads before the replay's scatters, no append
+// atomics.  An iteration's dependent chain is then: barrier -> gathers of r_k (and x_i)
+// -> shuffles, step -> scatters -> barrier.  The dirty-list append of a changed x_i (read
+// only after the launch) is issued between barrier arrival and wait.  After the last
+// iteration the last step is also added to the other buffer, so both buffers leave the
+// launch equal to r_{k0+iters} and the next launch has nothing to replay; nonzero steps
+// are counted in registers.  Same arithmetic as pcdm_packed_kernel (alg:PCD1
+// PAPER.md:177-186; eq:h(x) PAPER.md:214-216).
+template <int G, bool LOGISTIC, int TPB = kThreads>
+__global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) pcdm_packed1_kernel(PackedParams P) {
+    const int t = threadIdx.x & (G - 1);
+    const unsigned gm = gmask_of<G>();
+    const int src = (threadIdx.x & 31) & ~(G - 1);
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int pair0 = 2 * (t - 1);
+    unsigned bar_target = 0;
+    const int64_t tau = P.tau;
+    extern __shared__ float s_dyn[];
+    float* s_hot = s_dyn;                  // [nhot] r_k at the hot rows
+    int* s_hrow = (int*)(s_dyn + P.nhot);  // [nhot] hot row ids
+    const int nhot = P.nhot;
+    const bool cache = P.hot_cache != 0;
+    const bool has_slots = (int64_t)blockIdx.x * (blockDim.x / G) < tau;
+    if (nhot) {
+        for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
+        __syncthreads();
+    }
+    // the slot of iteration it and its block, loaded before the barrier of iteration it-1
+    // completes (S and A do not depend on r)
+    int i_pf = -1;
+    int4 c_pf = make_int4(0, 0, 0, 0);
+    auto prefetch = [&](int64_t it) {
+        i_pf = -1;
+        if (it < P.iters && gid < tau) {
+            i_pf = ld_stream_s32(P.slots + it * tau + gid);
+            if (i_pf >= 0)
+                c_pf = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i_pf * G + t) : ld_stream_v4(P.blocks + (int64_t)i_pf * G + t);
+        }
+    };
+    prefetch(0);
+    int4 c_prev = make_int4(0, 0, 0, 0);
+    float d_prev = 0.0f;
+    int len_prev = 0;
+    unsigned nzl = 0;
+    int xl_i = -1;  // changed column whose dirty-list append is pending
+
+    for (int64_t it = 0; it < P.iters; ++it) {
+        const int64_t k = P.k0 + it;
+        const float* rP = (k & 1) ? P.r1 : P.r0;
+        float* rQ = (k & 1) ? P.r0 : P.r1;
+        if (cache && has_slots) {
+            // the previous iteration's readers of s_hot passed the barrier's __syncthreads
+            for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hot[h] = ld_l2_f32(rP + s_hrow[h]);
+            __syncthreads();
+        }
+        const int i = i_pf;
+        const int4 c = c_pf;
+        // the gathers first: everything below overlaps their latency
+        // (issuing the plain-row gathers before the hot-row copy and reading the hot entries
+        // after it measured slower: medium 26.0 -> 38.6, skewed tau = 2^12 38.3 -> 50.6 ms per
+        // 1e4 iterations, profiles/r02_reg_replay_ab.jsonl)
+        float xi = 0.0f, ra = 0.0f, rb = 0.0f;
+        int len = 0;
+        if (i >= 0) {
+            // x_i may have been changed by iteration k-1 after the block was prefetched
+            if (t == 0) xi = P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : ld_l2_f32(P.x + i);
+            len = __shfl_sync(gm, c.y, src);
+            if (t > 0) {
+                if (pair0 < len) ra = gather_r(rP, c.x, s_hot, s_hrow, cache);
+                if (pair0 + 1 < len) rb = gather_r(rP, c.z, s_hot, s_hrow, cache);
+            }
+        }
+        // replay this group's step of iteration k-1 into Q, from registers
+        if (d_prev != 0.0f && t > 0) scatter_chunk(rQ, c_prev, pair0, len_prev, d_prev, s_hrow);
+        float d = 0.0f;
+        if (i >= 0) {
+            float acc = 0.0f;
+            if (t > 0) {
+                const float wa = pair0 < len ? grad_weight<LOGISTIC>(ra) : 0.0f;
+                const float wb = pair0 + 1 < len ? grad_weight<LOGISTIC>(rb) : 0.0f;
+                acc = fmaf(__int_as_float(c.y), wa, __int_as_float(c.w) * wb);
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gm, acc, o);
+            if (t == 0) {
+                const float xp = block_step<LOGISTIC>(xi, acc, P.beta * __int_as_float(c.x), P.lambda);
+                d = xp - xi;
+                if (d != 0.0f) {
+                    if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
+                    if (P.xlist) {
+                        ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
+                        if (P.xlist_cap > 0) xl_i = i;  // 0: dense iterate, no dirty list
+                    } else {
+                        P.x[i] = xp;
+                    }
+                    ++nzl;
+                }
+            }
+            d = __shfl_sync(gm, d, src);
+            if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+        }
+        c_prev = c;
+        d_prev = d;
+        len_prev = len;
+        if (P.cluster_sync) {
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        } else {
+            grid_arrive(P.barrier, bar_target);
+        }
+        prefetch(it + 1);
+        if (xl_i >= 0) {
+            const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
+            if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = xl_i;
+            xl_i = -1;
+        }
+        if (P.cluster_sync) {
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            grid_wait(P.barrier, bar_target);
+        }
+    }
+    // the last step into the other buffer as well (every gather of it passed the barrier)
+    if (d_prev != 0.0f && t > 0) {
+        float* rO = ((P.k0 + P.iters) & 1) ? P.r0 : P.r1;
+        scatter_chunk(rO, c_prev, pair0, len_prev, d_prev, s_hrow);
+    }
+    if (nzl) atomicAdd(P.nz_total, (unsigned long long)nzl);
+}
+
 // ---------------------------------------------------------------- asynchronous variant
 // What the paper's experiments ran: every worker repeatedly picks a
 // coordinate uniformly at random and updates it from whatever r currently holds, with
@@ -479,6 +613,8 @@ cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
     const int tpb = (ONE && P.cluster_sync == 2) ? 1024 : kThreads;
     const void* fn = tpb == 1024 ? (const void*)pcdm_packed_kernel<G, ONE, LOG, 1024>
                                  : (const void*)pcdm_packed_kernel<G, ONE, LOG>;
+    if (ONE && P.reg_replay)  // every group owns <= 1 slot per iteration: replay from registers
+        fn = tpb == 1024 ? (const void*)pcdm_packed1_kernel<G, LOG, 1024> : (const void*)pcdm_packed1_kernel<G, LOG>;
     const size_t smem = packed_smem_bytes(P.nhot, P.list_cap, P.hot_stage != 0);
     if (P.cluster_sync) {  // the whole grid is one cluster (ctas <= 16)
         if (ctas > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

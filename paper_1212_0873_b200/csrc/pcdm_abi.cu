@@ -1077,6 +1077,19 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     // cluster barrier instead of the global-memory grid barrier
     Q.cluster_sync = (packed || bat_fallback) && packed_plan.ctas <= 16 && !ragged_run ? cluster_sync : 0;
     if (ragged_run) Q.pipeline = 0;
+    // a grid that covers tau in one round (every group owns <= 1 slot per iteration: the
+    // latency-bound small-tau configs) replays the previous step from registers, without
+    // step lists (pcdm_packed1_kernel; iteration kernel per 1e4 iterations: medium 32.7 -> 22.7 ms, skewed
+    // tau = 2^8 35.2 -> 22.4, tau = 2^12 55.2 -> 35.8 ms;
+    // profiles/r02_reg_replay_ab.jsonl); PCDM_REG_REPLAY=0: the list-based loop
+    {
+        const int64_t groups = (int64_t)packed_plan.ctas * packed_plan.threads / std::max(1, p->packed_G);
+        const char* rr = knob("PCDM_REG_REPLAY");
+        Q.reg_replay = (packed || bat_fallback) && !ragged_run && one_barrier && !hot_stage && groups >= tau &&
+                               !(rr && atoi(rr) == 0)
+                           ? 1
+                           : 0;
+    }
     // cache the hot rows when the hottest one is read >= 1024 times per iteration
     // (tau count_max / n); below that the per-iteration copy costs more than the
     // same-address serialisation it removes (skewed, tau = 256: 55.2 vs 57.6 ms/step;

@@ -328,6 +328,34 @@ def test_packed_variant_both_barrier_schemes(gpu, monkeypatch, one_barrier, lens
                                    atol=1e-4 * np.max(np.abs(out["res"].r)))
 
 
+@pytest.mark.parametrize("iter_chunk", ["3", "64"], ids=["3-iteration-launches", "long-launches"])
+@pytest.mark.parametrize("reg_replay", ["1", "0"], ids=["register-replay", "list-replay"])
+def test_packed_one_slot_per_group(gpu, monkeypatch, reg_replay, iter_chunk):
+    # a grid that covers tau in one round: the previous iteration's step is replayed from
+    # the registers of the group that took it (pcdm_packed1_kernel, no step lists), both
+    # residual buffers equal at every launch boundary (3-iteration launches flip the
+    # buffer parity from launch to launch); the list-based loop on the same runs;
+    # dense nonzero starts (many steps per iteration), refreshes, idle slots
+    monkeypatch.setenv("PCDM_REG_REPLAY", reg_replay)
+    monkeypatch.setenv("PCDM_ITER_CHUNK", iter_chunk)
+    m, n = 5000, 4000
+    rng = np.random.default_rng(13)
+    lens = rng.integers(0, 30, size=n)
+    c, r, v, b, lam = _ragged(m, n, lens, 9, lam_frac=0.05)
+    x0 = np.random.default_rng(4).normal(size=n) * (np.arange(n) % 3 == 0)
+    nz = {}
+    for tau, iters, refresh, sampling in ((1, 200, 0, None), (64, 203, 0, None), (1000, 41, 7, None),
+                                          (4000, 6, -1, None), (700, 60, 0, ("binomial", 700, 0.6, None))):
+        out = run_both(c, r, v, b, lam, m, tau, iters, seed=tau, variant="packed", x0=x0,
+                       refresh_every=refresh, sampling=sampling)
+        assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
+        assert_parity(out)
+        np.testing.assert_allclose(out["r_gpu"], out["res"].r, rtol=0,
+                                   atol=1e-4 * np.max(np.abs(out["res"].r)))
+        nz[tau] = out["stats"]["nonzero_deltas"]
+    assert nz[1000] > 1000 and nz[64] > 0  # the step count survives the register form
+
+
 def test_long_columns_take_the_ragged_layout(gpu):
     # a column over 62 entries: the packed loop runs on the ragged layout (a CTA for the
     # long column, sub-warps for the rest); the uniform-only loops are rejected
