@@ -359,80 +359,79 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
         for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
         __syncthreads();
     }
-    // the slot of iteration it and its block, loaded before the barrier of iteration it-1
-    // completes (S and A do not depend on r)
-    int i_pf = -1;
-    int4 c_pf = make_int4(0, 0, 0, 0);
-    auto prefetch = [&](int64_t it) {
-        i_pf = -1;
-        if (it < P.iters && gid < tau) {
-            i_pf = ld_stream_s32(P.slots + it * tau + gid);
-            if (i_pf >= 0)
-                c_pf = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i_pf * G + t) : ld_stream_v4(P.blocks + (int64_t)i_pf * G + t);
-        }
+    // S and A do not depend on r: the slot id is loaded two iterations ahead and its block
+    // one iteration ahead (at the start of the iteration before), so neither load sits on
+    // the barrier-to-barrier chain (ncu on medium: the id -> block chain issued after the
+    // barrier arrival was 25 % of the warp samples)
+    const bool mine = gid < tau;
+    auto slot_of = [&](int64_t it) { return it < P.iters && mine ? ld_stream_s32(P.slots + it * tau + gid) : -1; };
+    auto block_of = [&](int col) {
+        if (col < 0) return make_int4(0, 0, 0, 0);  // idle: length 0
+        return P.xlist ? ld_l2_v4(P.blocks + (int64_t)col * G + t) : ld_stream_v4(P.blocks + (int64_t)col * G + t);
     };
-    prefetch(0);
+    int i_cur = slot_of(0);
+    int4 c_cur = block_of(i_cur);
+    int i_nx = slot_of(1);
     int4 c_prev = make_int4(0, 0, 0, 0);
     float d_prev = 0.0f;
     int len_prev = 0;
     unsigned nzl = 0;
     int xl_i = -1;  // changed column whose dirty-list append is pending
+    constexpr unsigned kFull = 0xffffffffu;  // every lane reaches the shuffles (idle groups carry zeros)
 
     for (int64_t it = 0; it < P.iters; ++it) {
         const int64_t k = P.k0 + it;
         const float* rP = (k & 1) ? P.r1 : P.r0;
         float* rQ = (k & 1) ? P.r0 : P.r1;
+        const int4 c_nx = block_of(i_nx);
+        const int i_nx2 = slot_of(it + 2);
         if (cache && has_slots) {
             // the previous iteration's readers of s_hot passed the barrier's __syncthreads
             for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hot[h] = ld_l2_f32(rP + s_hrow[h]);
             __syncthreads();
         }
-        const int i = i_pf;
-        const int4 c = c_pf;
+        const int i = i_cur;
+        const int4 c = c_cur;
+        const bool act = i >= 0;
         // the gathers first: everything below overlaps their latency
         // (issuing the plain-row gathers before the hot-row copy and reading the hot entries
         // after it measured slower: medium 26.0 -> 38.6, skewed tau = 2^12 38.3 -> 50.6 ms per
         // 1e4 iterations, profiles/r02_reg_replay_ab.jsonl)
         float xi = 0.0f, ra = 0.0f, rb = 0.0f;
-        int len = 0;
-        if (i >= 0) {
-            // x_i may have been changed by iteration k-1 after the block was prefetched
-            if (t == 0) xi = P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : ld_l2_f32(P.x + i);
-            len = __shfl_sync(gm, c.y, src);
-            if (t > 0) {
-                if (pair0 < len) ra = gather_r(rP, c.x, s_hot, s_hrow, cache);
-                if (pair0 + 1 < len) rb = gather_r(rP, c.z, s_hot, s_hrow, cache);
-            }
+        // x_i may have been changed by iteration k-1 after the block was loaded
+        if (act && t == 0) xi = P.xlist ? ld_l2_f32((const float*)(P.blocks + (int64_t)i * G) + 2) : ld_l2_f32(P.x + i);
+        const int len = __shfl_sync(kFull, c.y, src);
+        if (t > 0) {
+            if (pair0 < len) ra = gather_r(rP, c.x, s_hot, s_hrow, cache);
+            if (pair0 + 1 < len) rb = gather_r(rP, c.z, s_hot, s_hrow, cache);
         }
         // replay this group's step of iteration k-1 into Q, from registers
         if (d_prev != 0.0f && t > 0) scatter_chunk(rQ, c_prev, pair0, len_prev, d_prev, s_hrow);
-        float d = 0.0f;
-        if (i >= 0) {
-            float acc = 0.0f;
-            if (t > 0) {
-                const float wa = pair0 < len ? grad_weight<LOGISTIC>(ra) : 0.0f;
-                const float wb = pair0 + 1 < len ? grad_weight<LOGISTIC>(rb) : 0.0f;
-                acc = fmaf(__int_as_float(c.y), wa, __int_as_float(c.w) * wb);
-            }
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gm, acc, o);
-            if (t == 0) {
-                const float xp = block_step<LOGISTIC>(xi, acc, P.beta * __int_as_float(c.x), P.lambda);
-                d = xp - xi;
-                if (d != 0.0f) {
-                    if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
-                    if (P.xlist) {
-                        ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
-                        if (P.xlist_cap > 0) xl_i = i;  // 0: dense iterate, no dirty list
-                    } else {
-                        P.x[i] = xp;
-                    }
-                    ++nzl;
-                }
-            }
-            d = __shfl_sync(gm, d, src);
-            if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
+        float acc = 0.0f;
+        if (t > 0) {
+            const float wa = pair0 < len ? grad_weight<LOGISTIC>(ra) : 0.0f;
+            const float wb = pair0 + 1 < len ? grad_weight<LOGISTIC>(rb) : 0.0f;
+            acc = fmaf(__int_as_float(c.y), wa, __int_as_float(c.w) * wb);
         }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        float d = 0.0f;
+        if (act && t == 0) {
+            const float xp = block_step<LOGISTIC>(xi, acc, P.beta * __int_as_float(c.x), P.lambda);
+            d = xp - xi;
+            if (d != 0.0f) {
+                if (!isfinite(xp)) atomicOr(P.flags, FLAG_DIVERGED);
+                if (P.xlist) {
+                    ((float*)(P.blocks + (int64_t)i * G))[2] = xp;
+                    if (P.xlist_cap > 0) xl_i = i;  // 0: dense iterate, no dirty list
+                } else {
+                    P.x[i] = xp;
+                }
+                ++nzl;
+            }
+        }
+        d = __shfl_sync(kFull, d, src);
+        if (d != 0.0f && t > 0) scatter_chunk(rQ, c, pair0, len, d, s_hrow);
         c_prev = c;
         d_prev = d;
         len_prev = len;
@@ -441,12 +440,14 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
         } else {
             grid_arrive(P.barrier, bar_target);
         }
-        prefetch(it + 1);
         if (xl_i >= 0) {
             const unsigned long long q = atomicAdd(P.xlist_count, 1ull);
             if (q < (unsigned long long)P.xlist_cap) P.xlist[q] = xl_i;
             xl_i = -1;
         }
+        i_cur = i_nx;
+        c_cur = c_nx;
+        i_nx = i_nx2;
         if (P.cluster_sync) {
             asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         } else {

@@ -1079,8 +1079,8 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     if (ragged_run) Q.pipeline = 0;
     // a grid that covers tau in one round (every group owns <= 1 slot per iteration: the
     // latency-bound small-tau configs) replays the previous step from registers, without
-    // step lists (pcdm_packed1_kernel; iteration kernel per 1e4 iterations: medium 32.7 -> 22.7 ms, skewed
-    // tau = 2^8 35.2 -> 22.4, tau = 2^12 55.2 -> 35.8 ms;
+    // step lists (pcdm_packed1_kernel; iteration kernel per 1e4 iterations: medium 32.7 -> 20.4 ms, skewed
+    // tau = 2^8 35.2 -> 19.9, tau = 2^12 55.2 -> 38.8 ms;
     // profiles/r02_reg_replay_ab.jsonl); PCDM_REG_REPLAY=0: the list-based loop
     {
         const int64_t groups = (int64_t)packed_plan.ctas * packed_plan.threads / std::max(1, p->packed_G);
