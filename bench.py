@@ -40,7 +40,9 @@ from paper_1212_0873_b200 import instances as I  # noqa: E402
 METRIC = "coordinate updates/sec and effective GB/s (fraction of HBM/L2 roofline) at 1 B200"
 BYTES_PER_NNZ = 16  # val 4 + idx 4 + r gather 4 + r scatter 4
 VARIANT_NAMES = {1: "grid", 2: "smem", 3: "block", 4: "packed", 5: "batched", -1: "async"}
-KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem_kernel", 3: "pcdm_iter_kernel", 4: "pcdm_packed_kernel",
+KERNEL_OF_VARIANT = {1: "pcdm_iter_kernel", 2: "pcdm_smem1_kernel", 3: "pcdm_iter_kernel",
+                     4: "pcdm_packed_kernel (pcdm_packed1_kernel when the grid covers tau in one round, "
+                        "pcdm_ragged_kernel on the ragged layout)",
                      5: "batch_expand+batch_sweep+screen_test (+screen_fix on its own stream, under the next expand)",
                      -1: "pcdm_async_kernel"}
 # The oracle timing sample, per config (one definition for the cpu_baseline of our
@@ -239,7 +241,8 @@ def ncu_traffic(config, variant, sampling, iters_per_launch, tau=None):
         d = table.get("%s@%s:%s:%s" % (config, tau, variant, sampling)) or table["%s:%s:%s" % (config, variant, sampling)]
     except Exception:
         return None
-    out = {"dram": float(d["dram_bytes_per_iter"]) * iters_per_launch, "source": d.get("source")}
+    out = {"dram": float(d["dram_bytes_per_iter"]) * iters_per_launch, "source": d.get("source"),
+           "kernel": d.get("kernel")}
     if d.get("l2_bytes_per_iter") is not None:
         out["l2"] = float(d["l2_bytes_per_iter"]) * iters_per_launch
     return out
@@ -573,7 +576,8 @@ def bench_ours(args, world, rank, local):
                      "dram_traffic_frac_of_hbm": traffic["dram"] / (launch_ms / 1e3) / 1e9 / hpeak
                      if traffic else None,
                      "hbm_peak": hpeak,
-                     "kernel": KERNEL_OF_VARIANT.get(st0["variant"], "?"), "algorithmic_bytes_per_launch": alg_bytes_launch,
+                     "kernel": (traffic or {}).get("kernel") or KERNEL_OF_VARIANT.get(st0["variant"], "?"),
+                     "algorithmic_bytes_per_launch": alg_bytes_launch,
                      "launch_ms": launch_ms, "iters_per_launch": iters_per_launch,
                      "share_of_step": it_ms / max(sum(step_ms), 1e-9)},
         "breakdown_ms_per_step": {"iteration_kernel": it_ms / K, "sampler": samp_ms / K, "setup": setup_ms / K},

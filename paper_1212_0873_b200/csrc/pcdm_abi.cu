@@ -764,7 +764,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     const bool join_all = pjoin && atoi(pjoin) != 0;
     const bool per_pass = (pdev ? atoi(pdev) != 0 : true) && !join_all;
     const bool presample = (!x_dev || per_pass || join_all) && iters > 0 && spec.kind == PCDM_SAMPLING_NICE &&
-                           !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(2ll << 30);
+                           !(pe && atoi(pe) == 0) && (double)iters * (double)tau * 4.0 <= (double)(4ll << 30);
     // ragged layout: the slot arrays are binned by column class; with presampling the
     // binning rides on each sampler pass (side stream), else it runs before each launch
     const IterLaunch plan0 = plan_iter(variant >= PCDM_VARIANT_PACKED ? PCDM_VARIANT_GRID : variant, p->m, p->n,
