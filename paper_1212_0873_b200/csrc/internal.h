@@ -168,6 +168,8 @@ struct PackedParams {
                           //    cp.async.bulk (TMA engine) pieces, scattered from the staged copy
     int hot_stage;        // 1 (one-barrier scheme): scatters into hot rows accumulate in shared
                           //    memory per CTA, one red.global.add per hot row and CTA per iteration
+    int local_cap;        // > 0 (one-barrier scheme): each CTA keeps its own steps in shared memory (capacity
+                          //    per list) and replays them itself; no global step lists
     int reg_replay;       // 1 (one-barrier scheme, grid covers tau in one round): pcdm_packed1_kernel,
                           //    the previous step replayed from the registers of the group that took it
     // ragged layout (kernels_ragged.cu): per iteration the slots binned by class
@@ -220,10 +222,10 @@ cudaError_t launch_max_len(int64_t n, const int64_t* colptr, int* out, cudaStrea
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
                         const int* hot_rows, int nhot, int4* blocks, cudaStream_t st, int sms, int64_t* launches);
 int packed_ctas(int G, bool one_barrier, int sms, bool logistic = false, int nhot = 0, int list_cap = 0,
-                bool hot_stage = false);
+                bool hot_stage = false, int local_cap = 0);
 cudaError_t launch_packed(int G, bool one_barrier, int ctas, const PackedParams& P, cudaStream_t st,
                           int64_t* launches);
-size_t packed_smem_bytes(int nhot, int list_cap = 0, bool hot_stage = false);
+size_t packed_smem_bytes(int nhot, int list_cap = 0, bool hot_stage = false, int local_cap = 0);
 
 // ---- batched-snapshot loop (kernels_batched.cu): passes expand / sweep / steps / fold
 struct BatchedParams {

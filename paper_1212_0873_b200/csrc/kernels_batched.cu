@@ -1377,6 +1377,7 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
     // chunk's fix-up (one CTA that needs a whole SM), else two of its persistent CTAs would
     // start only after the fix-up and finish last
     const int esms = P.screen && sch && sms > 1 ? sms - 1 : sms;
+    if (const char* v = knob("PCDM_EXPAND_PER_SM")) per1 = std::max(1, std::min(per1, atoi(v)));
     const int g1 = std::min(P.nq, std::max(1, per1) * esms);
     batch_expand_kernel<G><<<g1, kExpandThreads, sm1, st>>>(P);
     // the sweep reads r and (for the speculative steps) x: after the previous fix-up
@@ -1385,16 +1386,21 @@ cudaError_t launch_all(const BatchedParams& P0, int ctas3, cudaStream_t st, int 
         if (e != cudaSuccess) return e;
     }
     // pass 2: groups of qpc slot ranges per CTA, g0 accumulated in shared memory
-    const int qpc = std::max(1, std::min(kSweepMaxSlots >> P.cq_log, (P.nq + 2 * sms - 1) / (2 * sms)));
+    int sweep_per_sm = 2, sweep_max = kSweepMaxSlots;
+    if (const char* v = knob("PCDM_SWEEP_PER_SM")) {
+        sweep_per_sm = std::max(1, std::min(2, atoi(v)));
+        if (sweep_per_sm == 1) sweep_max = 2 * kSweepMaxSlots;  // one CTA per SM: twice the accumulators
+    }
+    const int qpc = std::max(1, std::min(sweep_max >> P.cq_log, (P.nq + sweep_per_sm * sms - 1) / (sweep_per_sm * sms)));
     const size_t sm2 = ((size_t)qpc << P.cq_log) * sizeof(float) + ((size_t)1 << (kStaleLog - 3));
     const void* sw = P.logistic ? (const void*)batch_sweep_kernel<true> : (const void*)batch_sweep_kernel<false>;
     e = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     if (e != cudaSuccess) return e;
     const int ngrp = (P.nq + qpc - 1) / qpc;
     if (P.logistic)
-        batch_sweep_kernel<true><<<std::min(ngrp, 2 * sms), kThreads, sm2, st>>>(P, qpc);
+        batch_sweep_kernel<true><<<std::min(ngrp, sweep_per_sm * sms), kThreads, sm2, st>>>(P, qpc);
     else
-        batch_sweep_kernel<false><<<std::min(ngrp, 2 * sms), kThreads, sm2, st>>>(P, qpc);
+        batch_sweep_kernel<false><<<std::min(ngrp, sweep_per_sm * sms), kThreads, sm2, st>>>(P, qpc);
     if (P.screen) {
         const size_t smt = ((size_t)8 << kTestLog) + ((size_t)1 << (kTestBmLog - 3));
         e = cudaFuncSetAttribute(screen_test_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt);

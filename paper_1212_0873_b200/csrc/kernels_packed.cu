@@ -127,7 +127,12 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
     int* s_hrow = (int*)(s_dyn + P.nhot);      // [nhot] hot row ids
     const int nhot = P.nhot;
     // staged step list (P.list_cap > 0): [list_cap] ids, [list_cap] steps, count, base
-    const bool stage = P.list_cap > 0;
+    // CTA-local replay (P.local_cap > 0, one-barrier scheme): the slots of a CTA are the same
+    // positions of every iteration, so the CTA that took a step replays it; its steps stay in
+    // shared memory (3 rotating lists: append k%3, replay (k-1)%3, reset (k+1)%3), no global
+    // step list, no list counter to read after the barrier
+    const bool local = ONE_BARRIER && P.local_cap > 0;
+    const bool stage = !local && P.list_cap > 0;
     int* s_li = s_hrow + nhot;
     float* s_ld = (float*)(s_li + P.list_cap);
     int* s_lc = (int*)(s_ld + P.list_cap);
@@ -135,16 +140,36 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
     // staged hot-row scatters (P.hot_stage, one-barrier scheme): [nhot] accumulators
     float* s_hacc = stage ? (float*)(s_lbase + 1) : (float*)(s_hrow + nhot);
     const bool hstage = ONE_BARRIER && P.hot_stage && nhot > 0;
+    const int lcap = P.local_cap;
+    int* s_rcnt = (int*)(s_hacc + (P.hot_stage ? nhot : 0));  // [4]: 3 list counts
+    int* s_ri = s_rcnt + 4;                                    // [3][lcap] column ids
+    float* s_rd = (float*)(s_ri + 3 * lcap);                   // [3][lcap] steps
+    unsigned nzl = 0;                                          // thread 0: the CTA's nonzero steps
+    if (local && threadIdx.x < 3) s_rcnt[threadIdx.x] = 0;
     if (stage && threadIdx.x == 0) *s_lc = 0;
     if (hstage)
         for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hacc[h] = 0.0f;
     const bool cache = P.hot_cache != 0;
     // CTAs without slots in an iteration skip the hot-row copy
     const bool has_slots = (int64_t)blockIdx.x * (blockDim.x / G) < tau;
-    if (nhot || stage) {
+    if (nhot || stage || local) {
         for (int h = threadIdx.x; h < nhot; h += blockDim.x) s_hrow[h] = P.hot_rows[h];
         __syncthreads();
     }
+    // a step list of the CTA replayed into `dst` (a group of G lanes per entry)
+    auto replay_local = [&](int list, float* dst, bool staged) {
+        const int cnt = s_rcnt[list];
+        for (int e = threadIdx.x / G; e < cnt; e += blockDim.x / G) {
+            const int i = s_ri[list * lcap + e];
+            const float d = s_rd[list * lcap + e];
+            const int4 c = ld_stream_v4(P.blocks + (int64_t)i * G + t);
+            const int len = __shfl_sync(gm, c.y, src);
+            if (t > 0) {
+                if (staged) scatter_chunk_staged(dst, c, pair0, len, d, s_hrow, s_hacc);
+                else scatter_chunk(dst, c, pair0, len, d, s_hrow);
+            }
+        }
+    };
 
     // software pipeline: slot gid of iteration it and its block, loaded one iteration ahead
     int i_pf = -1;
@@ -165,8 +190,11 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
         const float* rP = (ONE_BARRIER && (k & 1)) ? P.r1 : P.r0;
         float* rQ = (ONE_BARRIER && (k & 1)) ? P.r0 : P.r1;
         const int* S = P.slots + it * tau;
-        if (blockIdx.x == 0 && threadIdx.x == 0) P.nz_count[next] = 0;
-        if (ONE_BARRIER) {
+        if (!local && blockIdx.x == 0 && threadIdx.x == 0) P.nz_count[next] = 0;
+        if (local) {
+            if (threadIdx.x == 0) s_rcnt[next] = 0;  // replayed in iteration k-1, before its barrier
+            replay_local(prev, rQ, hstage);
+        } else if (ONE_BARRIER) {
             // replay the previous iteration's nonzero steps into Q (first, so that its
             // dependent loads overlap phase A instead of following it)
             const int cntp = ld_l2_s32(P.nz_count + prev);
@@ -253,7 +281,11 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
                     } else {
                         P.x[i] = xp;
                     }
-                    if (stage) {  // CTA-local list, flushed with one global atomic per CTA
+                    if (local) {
+                        const int pos = atomicAdd(s_rcnt + cur, 1);
+                        s_ri[cur * lcap + pos] = i;
+                        s_rd[cur * lcap + pos] = d;
+                    } else if (stage) {  // CTA-local list, flushed with one global atomic per CTA
                         const int pos = atomicAdd(s_lc, 1);
                         s_li[pos] = i;
                         s_ld[pos] = d;
@@ -320,10 +352,18 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
             prefetch(it + 1);
             grid_wait(P.barrier, bar_target);
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (local) {
+            if (threadIdx.x == 0) nzl += (unsigned)s_rcnt[cur];  // complete since the barrier's __syncthreads
+        } else if (blockIdx.x == 0 && threadIdx.x == 0) {
             const int cnt = ld_l2_s32(P.nz_count + cur);
             if (cnt) atomicAdd(P.nz_total, (unsigned long long)cnt);
         }
+    }
+    if (local && P.iters > 0) {
+        // the last iteration's steps into the other buffer as well: both buffers leave the
+        // launch equal to r_{k0+iters}, the next launch has nothing to replay
+        replay_local((int)((P.k0 + P.iters - 1) % 3), ((P.k0 + P.iters) & 1) ? P.r0 : P.r1, false);
+        if (threadIdx.x == 0 && nzl) atomicAdd(P.nz_total, (unsigned long long)nzl);
     }
 }
 
@@ -616,7 +656,7 @@ cudaError_t launch_g(int ctas, const PackedParams& P, cudaStream_t st) {
                                  : (const void*)pcdm_packed_kernel<G, ONE, LOG>;
     if (ONE && P.reg_replay)  // every group owns <= 1 slot per iteration: replay from registers
         fn = tpb == 1024 ? (const void*)pcdm_packed1_kernel<G, LOG, 1024> : (const void*)pcdm_packed1_kernel<G, LOG>;
-    const size_t smem = packed_smem_bytes(P.nhot, P.list_cap, P.hot_stage != 0);
+    const size_t smem = packed_smem_bytes(P.nhot, P.local_cap > 0 ? 0 : P.list_cap, P.hot_stage != 0, P.local_cap);
     if (P.cluster_sync) {  // the whole grid is one cluster (ctas <= 16)
         if (ctas > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
@@ -710,9 +750,9 @@ cudaError_t launch_gather_list(const float* x, const int* list, int64_t count, f
     return cudaGetLastError();
 }
 
-size_t packed_smem_bytes(int nhot, int list_cap, bool hot_stage) {
+size_t packed_smem_bytes(int nhot, int list_cap, bool hot_stage, int local_cap) {
     return (size_t)nhot * (sizeof(float) + sizeof(int)) + (list_cap > 0 ? (size_t)list_cap * 8 + 8 : 0) +
-           (hot_stage ? (size_t)nhot * sizeof(float) : 0);
+           (hot_stage ? (size_t)nhot * sizeof(float) : 0) + (local_cap > 0 ? (size_t)local_cap * 24 + 16 : 0);
 }
 
 cudaError_t launch_pack(int64_t n, int G, const int64_t* colptr, const int* rowidx, const float* val, const float* L,
@@ -752,11 +792,12 @@ cudaError_t launch_async(int G, int ctas, const AsyncParams& A, cudaStream_t st,
     return cudaGetLastError();
 }
 
-int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot, int list_cap, bool hot_stage) {
+int packed_ctas(int G, bool one_barrier, int sms, bool logistic, int nhot, int list_cap, bool hot_stage,
+                int local_cap) {
     int per_sm = 1;
     const void* fn = logistic ? (one_barrier ? kernel_ptr<true, true>(G) : kernel_ptr<false, true>(G))
                               : (one_barrier ? kernel_ptr<true, false>(G) : kernel_ptr<false, false>(G));
-    const size_t smem = packed_smem_bytes(nhot, list_cap, hot_stage);
+    const size_t smem = packed_smem_bytes(nhot, list_cap, hot_stage, local_cap);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;

@@ -968,6 +968,24 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
                 list_cap = (int)cap;
         }
     }
+    // CTA-local replay (one-barrier scheme, uniform layout): a CTA's slots are the same
+    // positions of every iteration, so its steps stay in shared-memory lists and it replays
+    // them itself -- no global step lists, no list counter read after the barrier (large:
+    // profiles/r02_local_replay_ab.jsonl); taken when the lists fit 24 KB without lowering the
+    // occupancy; PCDM_LOCAL_REPLAY=0: the global lists
+    int local_cap = 0;
+    if (packed && !ragged_run && one_barrier) {
+        const char* lr = knob("PCDM_LOCAL_REPLAY");
+        const int64_t groups = (int64_t)plan.ctas * plan.threads / p->packed_G;
+        const int64_t cap = ((tau + groups - 1) / groups) * (plan.threads / p->packed_G);
+        if (!(lr && atoi(lr) == 0) && cap * 24 <= 24 * 1024 &&
+            (plan.threads != 512 ||
+             packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, 0, hot_stage, (int)cap) ==
+                 packed_ctas(p->packed_G, one_barrier, p->sms, p->loss == 1, p->nhot, 0, hot_stage))) {
+            local_cap = (int)cap;
+            list_cap = 0;
+        }
+    }
     const IterLaunch packed_plan = plan;  // the AUTO BATCHED fallback
     if (batched) packed = false;
     if (p->nz_cap < tau) {
@@ -1062,6 +1080,7 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
     Q.hot_rows = p->hot_rows;
     Q.nhot = p->nhot;
     Q.list_cap = list_cap;
+    Q.local_cap = local_cap;
     Q.hot_stage = hot_stage ? 1 : 0;
     Q.bulk_stage = ragged_run && bulk_stage ? 1 : 0;
     // software-pipelined slots when r is L2-resident (the loop is latency-bound there:

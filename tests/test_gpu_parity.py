@@ -356,6 +356,28 @@ def test_packed_one_slot_per_group(gpu, monkeypatch, reg_replay, iter_chunk):
     assert nz[1000] > 1000 and nz[64] > 0  # the step count survives the register form
 
 
+@pytest.mark.parametrize("iter_chunk", ["3", "64"], ids=["3-iteration-launches", "long-launches"])
+@pytest.mark.parametrize("local", ["1", "0"], ids=["cta-local-replay", "global-lists"])
+def test_packed_cta_local_replay(gpu, monkeypatch, local, iter_chunk):
+    # several slots per group (tau above the grid's groups) and one slot per group with
+    # the register form off: each CTA keeps its steps in shared-memory lists and replays
+    # them itself (no global step lists; both residual buffers equal at launch end),
+    # against the global-list loop on the same runs; dense nonzero starts, refreshes
+    monkeypatch.setenv("PCDM_LOCAL_REPLAY", local)
+    monkeypatch.setenv("PCDM_REG_REPLAY", "0")
+    monkeypatch.setenv("PCDM_ITER_CHUNK", iter_chunk)
+    m, n = 6000, 40_000
+    c, r, v, b, lam = _ragged(m, n, np.random.default_rng(2).integers(0, 14, size=n), 23, lam_frac=0.05)
+    x0 = np.random.default_rng(6).normal(size=n) * (np.arange(n) % 5 == 0)
+    for tau, iters, refresh in ((40_000, 7, 3), (30_000, 13, 0), (999, 41, 0), (64, 100, 7)):
+        out = run_both(c, r, v, b, lam, m, tau, iters, seed=tau, variant="packed", x0=x0, refresh_every=refresh)
+        assert out["stats"]["variant"] == pcdm.VARIANTS["packed"]
+        assert_parity(out)
+        np.testing.assert_allclose(out["r_gpu"], out["res"].r, rtol=0,
+                                   atol=1e-4 * np.max(np.abs(out["res"].r)))
+        assert out["stats"]["nonzero_deltas"] > 0
+
+
 def test_long_columns_take_the_ragged_layout(gpu):
     # a column over 62 entries: the packed loop runs on the ragged layout (a CTA for the
     # long column, sub-warps for the rest); the uniform-only loops are rejected
