@@ -73,7 +73,10 @@ typedef enum {
                                longer than 62 entries or would double every column's lanes,
                                the ragged layout: per sampled column 2..32 lanes, a warp
                                (63..1024 entries) or a CTA (longer) by its length, the
-                               slots binned by class after the sampler */
+                               slots binned by class after the sampler.  The previous
+                               iteration's steps are replayed into the second residual
+                               buffer from registers (grid covers tau in one round) or
+                               from CTA-local shared-memory lists */
     PCDM_VARIANT_BATCHED = 5, /* packed blocks; per chunk of iterations the partial
                                derivatives a_i^T r_0 of all sampled columns are computed at
                                once from the chunk's starting residual (gathers sorted by

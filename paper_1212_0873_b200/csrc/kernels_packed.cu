@@ -172,12 +172,16 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
     };
 
     // software pipeline: slot gid of iteration it and its block, loaded one iteration ahead
-    int i_pf = -1;
+    // (pipelined slot loop: also the id of the group's second slot, so that no block load
+    // waits for its slot id inside the loop)
+    int i_pf = -1, i_pf2 = -1;
     int4 c_pf = make_int4(0, 0, 0, 0);
     auto prefetch = [&](int64_t it) {
         i_pf = -1;
+        i_pf2 = -1;
         if (it < P.iters && gid < tau) {
             i_pf = ld_stream_s32(P.slots + it * tau + gid);
+            if (P.pipeline && gid + ngroups < tau) i_pf2 = ld_stream_s32(P.slots + it * tau + gid + ngroups);
             if (i_pf >= 0)
                 c_pf = P.xlist ? ld_l2_v4(P.blocks + (int64_t)i_pf * G + t) : ld_stream_v4(P.blocks + (int64_t)i_pf * G + t);
         }
@@ -230,26 +234,26 @@ __global__ void __launch_bounds__(TPB, TPB == kThreads ? PCDM_PACKED_MINB : 1) p
             return P.xlist ? ld_l2_v4(P.blocks + (int64_t)col * G + t) : ld_stream_v4(P.blocks + (int64_t)col * G + t);
         };
         const bool pipeline = P.pipeline != 0;
-        int i_nx = -1;
-        int4 c_nx = c_pf;
+        // pipelined: (i_cur, c_cur) = the slot being processed, i_n1 = the id of the next one
+        // (loaded a slot ago), whose block is issued now; the id after that is issued too
+        int i_cur = i_pf, i_n1 = i_pf2;
+        int4 c_cur = c_pf;
         for (int64_t j = gid; j < tau; j += ngroups) {
             const bool first = j == gid;
             int i;
             int4 c;
-            if (first) {
-                i = i_pf;
-                c = c_pf;
-            } else if (pipeline) {
-                i = i_nx;
-                c = c_nx;
+            if (first || pipeline) {
+                i = i_cur;
+                c = c_cur;
             } else {
                 i = ld_stream_s32(S + j);
                 if (i >= 0) c = load_block(i);
             }
             const int64_t jn = j + ngroups;
             if (pipeline && jn < tau) {
-                i_nx = ld_stream_s32(S + jn);
-                if (i_nx >= 0) c_nx = load_block(i_nx);
+                if (i_n1 >= 0) c_cur = load_block(i_n1);
+                i_cur = i_n1;
+                i_n1 = jn + ngroups < tau ? ld_stream_s32(S + jn + ngroups) : -1;
             }
             if (i < 0) continue;  // idle processor (non-nice samplings)
             float xi = 0.0f;

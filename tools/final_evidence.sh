@@ -18,4 +18,5 @@ python bench.py --impl reference --steps 3 --warmup 1 > $O/final_reference.json 
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-parity"
 $CMD > $O/final_plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'pcdm_|batch_|screen_|sample_|xhdr_|neg_b|scatter_x|round_r|residual_|objective_|row_counts|validate_|col_norms|pack_kernel|max_kernel|max_len|hot_cand|gather_list|check_finite' -c 1500 --csv --log-file $O/final_launches.csv $CMD > $O/final_ncu.log 2>&1
+tools/capture_config_traffic.sh "large 65536 pcdm_packed" "skewed 65536 pcdm_packed" > $O/final_capture.txt 2>&1
 tail -n 3 $O/final_pytest.txt; tail -n 2 $O/final_smoke.txt; wc -l $O/final_configs.jsonl; cut -c1-300 $O/final_bench_huge.json
