@@ -1124,10 +1124,11 @@ pcdm_status run_impl(pcdm_problem* p, float* x, const SamplingSpec& spec, int64_
         CK(cudaMalloc((void**)&tl_buf, 8 * 256 * sizeof(unsigned long long)), "alloc timeline");
         CK(cudaMemsetAsync(tl_buf, 0, 8 * 256 * sizeof(unsigned long long), st), "memset timeline");
     }
-    // BATCHED: iterations per snapshot (the passes' unit), its own rule independent of the
-    // sampler pass size: 18 (huge: the best of 9..36 with the sampler pass held fixed,
-    // profiles/r01_batched_chunk_ab.txt), at most one refresh period and the run
-    int64_t bchunk = 18;
+    // BATCHED: iterations per chunk (the passes' unit), its own rule independent of the
+    // sampler pass size: 16 (huge with the screened step pass: 15-16 beat 10-14 and 17-23 by
+    // ~3 %, 25+ needs a second wave of sweep CTAs, profiles/r02_batched_chunk_ab.txt; round 1
+    // chose 18 for the grid-barrier step pass), at most one refresh period and the run
+    int64_t bchunk = 16;
     if (const char* bc = knob("PCDM_BATCHED_CHUNK")) bchunk = std::max<int64_t>(1, atoll(bc));
     bchunk = std::min<int64_t>(bchunk, std::max<int64_t>(iters, 1));
     if (R > 0) bchunk = std::min(bchunk, R);
